@@ -1,0 +1,186 @@
+/*
+ * clover.h -- C-ABI of libclover_b200.so, the B200 (sm_100a) configuration-search
+ * hot path of Clover (arXiv 2304.09781).
+ *
+ * Plain C: pointers, sizes and PODs only; no torch types.  Every entry point
+ * returns a clv_status; non-zero codes map 1:1 onto the reference exception
+ * hierarchy (reference pkg/src/carbon_sched/errors.py:4-37) and
+ * clv_last_error() returns the message.  Device pointers (suffix _dev) are
+ * owned by the caller (cudaMalloc / torch.Tensor.data_ptr()); the context owns
+ * the tables and scratch.  One context per device; calls are stream-ordered on
+ * the cudaStream_t passed as `stream` (NULL = legacy default stream); calls
+ * that fill a host-side clv_best synchronise that stream.
+ *
+ * Reference interface each entry point replaces (SPEC = reference SPEC.md,
+ * mig.py / core.py = reference pkg/src/carbon_sched/):
+ *   clv_set_topology        MigTopology.__init__ / load_topology      mig.py:94-123, 201-217
+ *   clv_set_profile         ProfileTable / memory_feasible
+ *   clv_build_feasibility   MigTopology._partition_search (bulk)      mig.py:144-170
+ *   clv_feasible            is_feasible_fleet                         mig.py:179-181, 234
+ *   clv_realize             partition_fleet + realize                 mig.py:172-177
+ *   clv_score_graphs        evaluate() over ConfigGraphs, Eqs 1-3,6
+ *   clv_score_x             FleetConfig decode + evaluate             mig.py:237-299
+ *   clv_oracle_search       oracle_search
+ *   clv_anneal              anneal + sample_neighbor
+ *   clv_sweep               blover_search draws (x-space sweep)
+ *   clv_select_chains /
+ *   clv_reduce_records      best tracking / fixed-order winner
+ *   clv_derive_seed         derive_seed                               core.py:107-118
+ */
+#ifndef CLOVER_B200_H
+#define CLOVER_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CLV_ABI_VERSION 1
+#define CLV_MAX_VARIANTS 8
+#define CLV_MAX_EDGES 40
+#define CLV_MAX_CONFIGS 32
+#define CLV_MAX_FAMILIES 8
+#define CLV_MAX_PODS 8
+
+typedef enum clv_status {
+    CLV_OK = 0,
+    CLV_ERR_CARBON_SCHED = 1,          /* CarbonSchedError            errors.py:4  */
+    CLV_ERR_INVALID_CONFIG = 2,        /* InvalidConfigError          errors.py:8  */
+    CLV_ERR_INFEASIBLE_ASSIGNMENT = 3, /* InfeasibleAssignmentError   errors.py:12 */
+    CLV_ERR_INCOMPATIBLE_GRAPHS = 4,   /* IncompatibleGraphsError     errors.py:16 */
+    CLV_ERR_INFEASIBLE_GRAPH = 5,      /* InfeasibleGraphError        errors.py:20 */
+    CLV_ERR_NO_NEIGHBOR = 6,           /* NoNeighborError             errors.py:24 */
+    CLV_ERR_PROFILE = 7,               /* ProfileError                errors.py:28 */
+    CLV_ERR_TRACE = 8,                 /* TraceError                  errors.py:32 */
+    CLV_ERR_SIMULATION = 9,            /* SimulationError             errors.py:36 */
+    CLV_ERR_CUDA = 100,
+    CLV_ERR_OUT_OF_MEMORY = 101,
+    CLV_ERR_NOT_READY = 102            /* tables / topology / feasibility not loaded */
+} clv_status;
+
+typedef struct clv_ctx clv_ctx;
+
+/* Evaluation parameters of one scoring call (ObjectiveParams core.py:63-101 + workload). */
+typedef struct clv_eval_params {
+    double arrival_rps;      /* R: Poisson request rate                */
+    double ci;               /* carbon intensity, gCO2/kWh           */
+    double carbon_weight;    /* lambda of Eq. 3, clamped to [0,1]                 */
+    double base_accuracy;    /* A_base of Eq. 1 (fraction)                       */
+    double base_carbon_g;    /* C_base of Eq. 2 (gCO2/request)                   */
+    double latency_slo_ms;   /* L_tail of Eq. 5                                  */
+    double rho_sat;          /* queueing-factor saturation (0.999)               */
+    int32_t strict_eq6;      /* 1 = verbatim Eq. 6 (CARBON_SCHED_STRICT_EQ6)     */
+    int32_t n_gpus;          /* fleet size n                                     */
+} clv_eval_params;
+
+/* Selected candidate of a scoring / search call. */
+typedef struct clv_best {
+    int64_t index;           /* candidate index (global), -1 if none            */
+    double f, h, p95_ms, accuracy, energy_wh;
+    int32_t sla_met;
+    int32_t found;           /* 1 if at least one valid candidate was scored     */
+    int64_t valid_count;     /* candidates that were feasible and scored         */
+    int64_t sla_count;       /* of those, SLA-meeting                            */
+} clv_best;
+
+/* Selection rules (SPEC:464/482-483 vs SPEC:539/548). */
+#define CLV_SELECT_BEST_H 0  /* (SLA desc, h asc, index asc)                                 */
+#define CLV_SELECT_ORACLE 1  /* (SLA desc, f desc, index asc), none SLA: (p95 asc, index asc) */
+
+/* Annealing schedule. */
+typedef struct clv_anneal_params {
+    double t_init, cooling_step, t_floor;
+    int32_t stall_limit;
+    int32_t max_steps;
+    int32_t proposal;        /* 0 = best-h neighbour, 1 = uniform (min-hash) neighbour */
+    int32_t evaluate;        /* 0 = score whole neighbourhood, 1 = score proposal only */
+} clv_anneal_params;
+
+/* Per-chain result written by clv_anneal (device memory). */
+typedef struct clv_chain_result {
+    double f, h, p95_ms, accuracy, energy_wh;   /* best candidate */
+    int32_t sla_met;
+    int32_t status;          /* 0 max_steps, 1 stalled, 2 no neighbour, -1 invalid start */
+    int32_t steps;
+    int32_t best_step;       /* -1 = the start graph */
+    int64_t best_index;      /* canonical neighbour index at best_step, -1 = start */
+    int64_t evals;           /* candidates scored by this chain (start included) */
+} clv_chain_result;
+
+/* One row of the optional per-step log (SPEC:487 schema). */
+typedef struct clv_log_row {
+    double temp, f, h, p95_ms;
+    int32_t iter, ged_from_center, sla_met, accepted, new_best, pad;
+} clv_log_row;
+
+/* 32-byte winner record exchanged between ranks (one per GPU per round). */
+typedef struct clv_record {
+    uint64_t k1;             /* 0 = SLA met, 1 = not (lexicographic primary)      */
+    uint64_t k2;             /* order-preserving key of h                          */
+    int64_t index;           /* global chain / candidate index                    */
+    double h;
+} clv_record;
+
+/* One pod of a mixed-family sweep. */
+typedef struct clv_pod {
+    int32_t family;
+    int32_t n_gpus;
+    double weight;
+    clv_eval_params params;
+} clv_pod;
+
+int clv_abi_version(void);
+int clv_create(int device, clv_ctx **out);
+void clv_destroy(clv_ctx *ctx);
+const char *clv_last_error(const clv_ctx *ctx);
+uint64_t clv_derive_seed(const uint64_t *parts, int n_parts);
+
+int clv_set_topology(clv_ctx *ctx, int n_configs, const int32_t *config_ids,
+                     const int32_t *counts5, const double *memory_gb5);
+int clv_set_profile(clv_ctx *ctx, int family, int n_variants,
+                    const int64_t *thr_q, const int64_t *acc_q, const int64_t *en_q,
+                    const int64_t *idle_q5, const double *lat95, const uint8_t *mem_ok,
+                    int kt, int ke, int ki);
+int clv_build_feasibility(clv_ctx *ctx, int n_max, void *stream);
+int64_t clv_feasibility_bytes(const clv_ctx *ctx);
+
+int clv_feasible(clv_ctx *ctx, int n, const int32_t *vec5_dev, int64_t count,
+                 uint8_t *out_dev, void *stream);
+int clv_realize(clv_ctx *ctx, int n, const int32_t *vec5_host, int32_t *partitions_host,
+                void *stream);
+
+int clv_score_graphs(clv_ctx *ctx, int family, const uint16_t *w_dev, int64_t count,
+                     int64_t index_base, const clv_eval_params *params, int select_mode,
+                     double *f_dev, double *h_dev, uint8_t *sla_dev, uint8_t *feasible_dev,
+                     double *p95_dev, clv_best *best, void *stream);
+int clv_score_x(clv_ctx *ctx, int family, int n, const uint8_t *xp_dev,
+                const uint8_t *xv_dev, const int64_t *xv_offsets_dev, int64_t count,
+                int64_t index_base, const clv_eval_params *params, int select_mode,
+                double *f_dev, double *h_dev, uint8_t *sla_dev, clv_best *best, void *stream);
+int clv_oracle_search(clv_ctx *ctx, int family, int n, int64_t begin, int64_t end,
+                      const clv_eval_params *params, clv_best *best, int64_t *total,
+                      void *stream);
+int clv_oracle_size(clv_ctx *ctx, int family, int64_t *total);
+int clv_oracle_decode(clv_ctx *ctx, int family, int64_t index, int32_t *config_id,
+                      int32_t *assignment7, int32_t *n_slices);
+int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base,
+               const uint16_t *start_w_dev, const clv_eval_params *params, int n_params,
+               const clv_anneal_params *ap, uint64_t seed, int cluster_size,
+               clv_chain_result *results_dev, uint16_t *best_w_dev, uint16_t *final_w_dev,
+               clv_log_row *log_dev, void *stream);
+int clv_select_chains(clv_ctx *ctx, const clv_chain_result *results_dev, int n_chains,
+                      int64_t chain_base, clv_record *record_dev, void *stream);
+int clv_reduce_records(clv_ctx *ctx, const clv_record *records_dev, int count,
+                       clv_record *out_dev, void *stream);
+int clv_sweep(clv_ctx *ctx, int n_pods, const clv_pod *pods, int64_t begin, int64_t end,
+              uint64_t seed, double *f_dev, double *h_dev, uint8_t *sla_dev,
+              clv_best *best, void *stream);
+int clv_sweep_decode(clv_ctx *ctx, int n_pods, const clv_pod *pods, uint64_t seed,
+                     int64_t index, int32_t *partitions_host, int32_t *assignments_host,
+                     int32_t *n_assignments);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CLOVER_B200_H */

@@ -1,0 +1,102 @@
+"""ORACLE -- TEST INFRASTRUCTURE ONLY.  The table-surrogate evaluator.
+
+Restates DESIGN.md "Scoring surrogate" (the replacement for SPEC:334-372's DES,
+SURVEY 7.2 D1) and SPEC-literal Eqs. 1, 2, 3, 6 in numpy.
+Aggregates are recomputed from scratch per candidate (W @ rows, int64), so this
+is independent of the device's incremental neighbour scoring.  Every fp64
+operation is one IEEE-rounded numpy ufunc in the documented order; the kernels
+compile with -fmad=false and reproduce the same bits.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .tables import OracleTables
+
+
+@dataclass
+class Evaluated:
+    A: np.ndarray
+    E: np.ndarray
+    L: np.ndarray
+    f: np.ndarray
+    h: np.ndarray
+    sla: np.ndarray
+
+
+def constants(tables: OracleTables, scenario):
+    R = float(scenario.arrival_rps)
+    return dict(R_q=math.ldexp(R, tables.kt), inv_3600R=1.0 / (3600.0 * R),
+                en_scale=math.ldexp(1.0, tables.kt - tables.ke),
+                idle_scale=math.ldexp(1.0, -tables.ki))
+
+
+def aggregates(W: np.ndarray, tables: OracleTables):
+    W = np.asarray(W, dtype=np.int64).reshape(-1, tables.E)
+    s_thr = W @ tables.thr_q
+    s_acc = W @ tables.acc_q
+    s_en = W @ tables.en_q
+    cnt = W.reshape(len(W), tables.V, 5).sum(axis=1)
+    s_idle = cnt @ tables.idle_q
+    lmax = np.where(W > 0, tables.lat95[None, :], -np.inf).max(axis=1)
+    return s_thr, s_acc, s_en, s_idle, lmax
+
+
+def epilogue(s_thr, s_acc, s_en, s_idle, lmax, tables, scenario) -> Evaluated:
+    c = constants(tables, scenario)
+    obj = scenario.obj
+    a_base, c_base, slo = obj.base_accuracy, obj.base_carbon_g, obj.latency_slo_ms
+    lam, ci = obj.carbon_weight, float(scenario.ci)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        thr_d = s_thr.astype(np.float64)
+        A = s_acc.astype(np.float64) / thr_d
+        rho = c["R_q"] / thr_d
+        e_act = (s_en.astype(np.float64) / thr_d) * c["en_scale"]
+        rho_c = np.minimum(rho, 1.0)
+        p_idle = s_idle.astype(np.float64) * c["idle_scale"]
+        E = e_act + ((1.0 - rho_c) * p_idle) * c["inv_3600R"]
+        rho_q = np.minimum(rho, scenario.rho_sat)
+        L = lmax / (1.0 - rho_q)
+        dA = (A - a_base) / a_base * 100.0
+        dC = (c_base - E / 1000.0 * ci) / c_base * 100.0
+        f = lam * dC + (1.0 - lam) * dA
+        sla = L <= slo
+        soft = np.where((f >= 0) | bool(scenario.strict_eq6), -f * (slo / L), -f * (L / slo))
+        h = np.where(sla, -f, soft)
+    return Evaluated(A, E, L, f, h, sla)
+
+
+def evaluate(W, tables: OracleTables, scenario) -> Evaluated:
+    return epilogue(*aggregates(W, tables), tables, scenario)
+
+
+def evaluate_one(w, tables, scenario) -> dict:
+    ev = evaluate(np.asarray(w)[None, :], tables, scenario)
+    return {k: (bool(getattr(ev, k)[0]) if k == "sla" else float(getattr(ev, k)[0]))
+            for k in ("A", "E", "L", "f", "h", "sla")}
+
+
+def base_graph(V: int, n: int) -> np.ndarray:
+    """BASE: largest variant on every unpartitioned GPU."""
+    w = np.zeros(V * 5, dtype=np.int64)
+    w[(V - 1) * 5 + 0] = n
+    return w
+
+
+def calibrate(profile, tables: OracleTables, n: int, ci: float, lam: float = 0.5,
+              utilization: float = 0.7, ci_base=None, strict: bool = False, pue: float = 1.5):
+    """R = utilization x BASE capacity; A_base, C_base, L_tail from BASE
+    (C_base without PUE per SURVEY D7)."""
+    from paper_2304_09781_b200.core import ObjectiveParams, SliceType
+    from paper_2304_09781_b200.objective import Scenario
+    V = profile.variant_count
+    R = utilization * n * (1000.0 / profile.mean_service_ms(V, SliceType.S7G))
+    probe = Scenario(n, R, float(ci), ObjectiveParams(1.0, 1.0, 1.0, lam, pue), strict)
+    ev = evaluate_one(base_graph(V, n), tables, probe)
+    cb = float(ci if ci_base is None else ci_base)
+    obj = ObjectiveParams(ev["A"], ev["E"] / 1000.0 * cb, ev["L"], lam, pue)
+    return Scenario(n, R, float(ci), obj, strict)

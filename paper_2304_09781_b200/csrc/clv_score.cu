@@ -1,0 +1,428 @@
+// clv_score.cu -- materialized-candidate scoring (K1+K2+K4), the exhaustive
+// ORACLE enumeration (K7), the counter-RNG x-space sweep (K7) and the chain /
+// rank winner reductions.
+//
+//  score_graphs : uint16 graph rows (E = 5V per row) streamed from HBM through a
+//                 shared-memory tile, exact int64 aggregates, fp64 epilogue,
+//                 fleet-feasibility lookup, grid argmax.       HBM/issue bound
+//  score_x      : FleetConfig (x^p, x^v) CSR rows decoded by one warp each
+//                 (shuffle prefix-sum of slices per GPU, mig.py:286-296)
+//  oracle       : index -> (config id, mixed-radix variant digits)
+//  sweep        : index -> counter-RNG draws -> per-pod graphs
+#include "clv_internal.h"
+
+namespace clv {
+
+constexpr int SNT = 256;
+
+struct __align__(16) ERow {
+    long long thr, acc, en, idle;
+};
+
+__device__ inline void stage_rows(ERow *row, double *lat_by_rank, unsigned char *rank,
+                                  const FamilyTables &T) {
+    for (int e = threadIdx.x; e < T.E; e += blockDim.x) {
+        row[e].thr = T.thr_q[e];
+        row[e].acc = T.acc_q[e];
+        row[e].en = T.en_q[e];
+        row[e].idle = T.idle_q[e % 5];
+        lat_by_rank[e] = T.lat_by_rank[e];
+        rank[e] = T.rank[e];
+    }
+}
+
+__device__ inline void consider(RecP &r0, RecP &r1, const Score &sc, long long idx, int mode) {
+    RecP c;
+    c.f = sc.f; c.L = sc.L; c.A = sc.A; c.E = sc.E; c.sla = sc.sla;
+    c.r.idx = idx; c.r.mv = 0u; c.r.hv = sc.h;
+    if (mode == CLV_SELECT_BEST_H) {
+        c.r.k1 = sc.sla ? 0u : 1u;
+        c.r.k2 = okey(sc.h);
+        if (rec_less(c.r, r0.r)) r0 = c;
+    } else {
+        if (sc.sla) {
+            c.r.k1 = 0u;
+            c.r.k2 = ~okey(sc.f);
+            if (rec_less(c.r, r0.r)) r0 = c;
+        }
+        c.r.k1 = 0u;
+        c.r.k2 = okey(sc.L);
+        if (rec_less(c.r, r1.r)) r1 = c;
+    }
+}
+
+// ------------------------------------------------------------ score_graphs
+template <bool VEC>
+__global__ void __launch_bounds__(SNT) score_graphs_kernel(const __grid_constant__ ScoreArgs a) {
+    __shared__ ERow row[CLV_MAX_EDGES];
+    __shared__ double lat_by_rank[CLV_MAX_EDGES];
+    __shared__ unsigned char rank[CLV_MAX_EDGES];
+    __shared__ __align__(16) uint16_t tile[SNT * CLV_MAX_EDGES];
+    const FamilyTables &T = *a.fam;
+    stage_rows(row, lat_by_rank, rank, T);
+    const int E = T.E;
+    const unsigned long long mem_ok = T.mem_ok;
+    const int n = a.ec.n;
+    RecP r0 = recp_none(), r1 = recp_none();
+    unsigned long long c_valid = 0, c_sla = 0;
+    __syncthreads();
+    for (long long base = (long long)blockIdx.x * SNT; base < a.count; base += (long long)gridDim.x * SNT) {
+        const long long rows = (a.count - base) < SNT ? (a.count - base) : SNT;
+        const uint16_t *src = a.w + base * E;
+        if (VEC) {
+            const int nvec = (int)((rows * E * 2) / 16);
+            const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+            uint4 *t4 = reinterpret_cast<uint4 *>(tile);
+            for (int q = threadIdx.x; q < nvec; q += SNT) t4[q] = __ldcs(s4 + q);
+            for (int q = nvec * 8 + threadIdx.x; q < rows * E; q += SNT) tile[q] = src[q];
+        } else {
+            for (int q = threadIdx.x; q < rows * E; q += SNT) tile[q] = src[q];
+        }
+        __syncthreads();
+        if (threadIdx.x < rows) {
+            const uint16_t *w = tile + threadIdx.x * E;
+            long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+            int sv[CLV_K] = {0, 0, 0, 0, 0};
+            unsigned long long m = 0;
+            bool memfail = false;
+            for (int e = 0; e < E; ++e) {
+                const long long x = w[e];
+                if (x) {
+                    S0 += x * row[e].thr; S1 += x * row[e].acc; S2 += x * row[e].en; S3 += x * row[e].idle;
+                    sv[e % 5] += (int)x;
+                    m |= 1ULL << rank[e];
+                    memfail |= !((mem_ok >> e) & 1ULL);
+                }
+            }
+            const long long i = base + threadIdx.x;
+            const bool feas = !memfail && m != 0 && feasible(a.F, n, sv[0], sv[1], sv[2], sv[3], sv[4]);
+            if (feas) {
+                Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)], a.ec);
+                ++c_valid;
+                c_sla += sc.sla;
+                consider(r0, r1, sc, a.index_base + i, a.select_mode);
+                if (a.f_out) a.f_out[i] = sc.f;
+                if (a.h_out) a.h_out[i] = sc.h;
+                if (a.p95_out) a.p95_out[i] = sc.L;
+                if (a.sla_out) a.sla_out[i] = sc.sla;
+            } else {
+                const double nan = __longlong_as_double(0x7FF8000000000000LL);
+                if (a.f_out) a.f_out[i] = nan;
+                if (a.h_out) a.h_out[i] = nan;
+                if (a.p95_out) a.p95_out[i] = nan;
+                if (a.sla_out) a.sla_out[i] = 0;
+            }
+            if (a.feas_out) a.feas_out[i] = feas;
+        }
+        __syncthreads();
+    }
+    grid_finish<SNT>(r0, r1, c_valid, c_sla, a.sel);
+}
+
+cudaError_t launch_score_graphs(const ScoreArgs &a, int grid, cudaStream_t s) {
+    const int E = 0;  (void)E;
+    bool vec = (reinterpret_cast<uintptr_t>(a.w) % 16) == 0;
+    if (vec) score_graphs_kernel<true><<<grid, SNT, 0, s>>>(a);
+    else score_graphs_kernel<false><<<grid, SNT, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------- score_x
+// One warp per candidate; lanes stride the GPUs, a shuffle scan of slice
+// counts gives each GPU's first assignment slot (FleetConfig layout, mig.py:240-242).
+__global__ void __launch_bounds__(SNT) score_x_kernel(const __grid_constant__ ScoreArgs a, int n) {
+    __shared__ ERow row[CLV_MAX_EDGES];
+    __shared__ double lat_by_rank[CLV_MAX_EDGES];
+    __shared__ unsigned char rank[CLV_MAX_EDGES];
+    __shared__ short row_of_id[256];
+    __shared__ unsigned char nsl[CLV_MAX_CONFIGS];
+    __shared__ unsigned char kinds[CLV_MAX_CONFIGS][8];
+    const FamilyTables &T = *a.fam;
+    const Topology &P = *a.topo;
+    stage_rows(row, lat_by_rank, rank, T);
+    for (int t = threadIdx.x; t < 256; t += SNT) row_of_id[t] = -1;
+    __syncthreads();
+    for (int r = threadIdx.x; r < P.K; r += SNT) {
+        if (P.ids[r] >= 0 && P.ids[r] < 256) row_of_id[P.ids[r]] = (short)r;
+        nsl[r] = (unsigned char)P.nslices[r];
+        for (int j = 0; j < 8; ++j) kinds[r][j] = P.kinds[r][j];
+    }
+    __syncthreads();
+    const int V = T.V;
+    const unsigned long long mem_ok = T.mem_ok;
+    const int lane = threadIdx.x & 31;
+    const long long warp0 = ((long long)blockIdx.x * SNT + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * SNT) >> 5;
+    RecP r0 = recp_none(), r1 = recp_none();
+    unsigned long long c_valid = 0, c_sla = 0;
+    for (long long c = warp0; c < a.count; c += nwarps) {
+        const uint8_t *xp = a.xp + c * n;
+        const long long off0 = a.xv_off[c], off1 = a.xv_off[c + 1];
+        long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+        unsigned long long m = 0;
+        int err = 0;
+        long long carry = 0;   // slots used by earlier 32-GPU chunks
+        for (int g0 = 0; g0 < n; g0 += 32) {
+            const int g = g0 + lane;
+            int r = -1, ns = 0;
+            if (g < n) {
+                r = row_of_id[xp[g]];
+                if (r < 0) err = CLV_ERR_INVALID_CONFIG; else ns = nsl[r];
+            }
+            int incl = ns;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                int y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= d) incl += y;
+            }
+            const long long pos = off0 + carry + (incl - ns);
+            for (int j = 0; j < ns; ++j) {
+                const long long q = pos + j;
+                if (q >= off1) { err = CLV_ERR_CARBON_SCHED; break; }
+                const int v = a.xv[q];
+                const int k = kinds[r][j];
+                if (v < 1 || v > V) { err = CLV_ERR_INFEASIBLE_ASSIGNMENT; break; }
+                const int e = (v - 1) * 5 + k;
+                if (!((mem_ok >> e) & 1ULL)) { err = CLV_ERR_INFEASIBLE_ASSIGNMENT; break; }
+                S0 += row[e].thr; S1 += row[e].acc; S2 += row[e].en; S3 += row[e].idle;
+                m |= 1ULL << rank[e];
+            }
+            carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            S0 += __shfl_xor_sync(0xFFFFFFFFu, S0, d);
+            S1 += __shfl_xor_sync(0xFFFFFFFFu, S1, d);
+            S2 += __shfl_xor_sync(0xFFFFFFFFu, S2, d);
+            S3 += __shfl_xor_sync(0xFFFFFFFFu, S3, d);
+            m |= __shfl_xor_sync(0xFFFFFFFFu, m, d);
+            int e2 = __shfl_xor_sync(0xFFFFFFFFu, err, d);
+            err = err ? err : e2;
+        }
+        if (lane == 0) {
+            if (!err && carry != off1 - off0) err = CLV_ERR_CARBON_SCHED;   // length mismatch
+            if (err) {
+                if (atomicCAS(a.error_flag, 0, err) == 0) *a.error_index = c;
+                if (a.sla_out) a.sla_out[c] = 0;
+            } else {
+                Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)], a.ec);
+                ++c_valid;
+                c_sla += sc.sla;
+                consider(r0, r1, sc, a.index_base + c, a.select_mode);
+                if (a.f_out) a.f_out[c] = sc.f;
+                if (a.h_out) a.h_out[c] = sc.h;
+                if (a.sla_out) a.sla_out[c] = sc.sla;
+            }
+        }
+    }
+    grid_finish<SNT>(r0, r1, c_valid, c_sla, a.sel);
+}
+
+cudaError_t launch_score_x(const ScoreArgs &a, int n, int grid, cudaStream_t s) {
+    score_x_kernel<<<grid, SNT, 0, s>>>(a, n);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ oracle
+__global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ OracleArgs a) {
+    __shared__ ERow row[CLV_MAX_EDGES];
+    __shared__ double lat_by_rank[CLV_MAX_EDGES];
+    __shared__ unsigned char rank[CLV_MAX_EDGES];
+    __shared__ unsigned char flist[CLV_K][CLV_MAX_VARIANTS];
+    const FamilyTables &T = *a.fam;
+    const Topology &P = *a.topo;
+    stage_rows(row, lat_by_rank, rank, T);
+    for (int t = threadIdx.x; t < CLV_K * CLV_MAX_VARIANTS; t += SNT)
+        flist[t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS] = T.feas_list[t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS];
+    __syncthreads();
+    const long long n = a.n;
+    RecP r0 = recp_none(), r1 = recp_none();
+    unsigned long long c_valid = 0, c_sla = 0;
+    for (long long i = a.begin + (long long)blockIdx.x * SNT + threadIdx.x; i < a.end;
+         i += (long long)gridDim.x * SNT) {
+        int r = 0;
+        while (r + 1 < P.K && a.row_off[r + 1] <= i) ++r;
+        long long rem = i - a.row_off[r];
+        long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+        unsigned long long m = 0;
+        const int ns = P.nslices[r];
+        for (int j = 0; j < ns; ++j) {
+            const int pl = a.row_place[r][j];
+            const int dgt = (int)(rem / pl);
+            rem -= (long long)dgt * pl;
+            const int k = P.kinds[r][j];
+            const int e = flist[k][dgt] * 5 + k;
+            S0 += row[e].thr; S1 += row[e].acc; S2 += row[e].en; S3 += row[e].idle;
+            m |= 1ULL << rank[e];
+        }
+        Score sc = epilogue(S0 * n, S1 * n, S2 * n, S3 * n, lat_by_rank[63 - __clzll((long long)m)], a.ec);
+        ++c_valid;
+        c_sla += sc.sla;
+        consider(r0, r1, sc, i, CLV_SELECT_ORACLE);
+    }
+    grid_finish<SNT>(r0, r1, c_valid, c_sla, a.sel);
+}
+
+cudaError_t launch_oracle(const OracleArgs &a, int grid, cudaStream_t s) {
+    oracle_kernel<<<grid, SNT, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- sweep
+struct Draws {
+    uint64_t h0, word;
+    uint32_t j;
+    __device__ inline uint32_t next() {
+        uint32_t out;
+        if ((j & 1u) == 0) { word = stream_word(h0, j >> 1); out = (uint32_t)word; }
+        else out = (uint32_t)(word >> 32);
+        ++j;
+        return out;
+    }
+    __device__ inline int bounded(uint32_t k) {
+        return (int)(((uint64_t)next() * k) >> 32);
+    }
+};
+
+__global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ SweepArgs a) {
+    __shared__ ERow row[CLV_MAX_PODS][CLV_MAX_EDGES];
+    __shared__ double lat_by_rank[CLV_MAX_PODS][CLV_MAX_EDGES];
+    __shared__ unsigned char rank[CLV_MAX_PODS][CLV_MAX_EDGES];
+    __shared__ unsigned char nfeas[CLV_MAX_PODS][CLV_K];
+    __shared__ unsigned char flist[CLV_MAX_PODS][CLV_K][CLV_MAX_VARIANTS];
+    __shared__ unsigned char nsl[CLV_MAX_CONFIGS];
+    __shared__ unsigned char kinds[CLV_MAX_CONFIGS][8];
+    const Topology &P = *a.topo;
+    for (int p = 0; p < a.n_pods; ++p) {
+        const FamilyTables &T = a.fam[a.pods[p].family];
+        stage_rows(row[p], lat_by_rank[p], rank[p], T);
+        for (int t = threadIdx.x; t < CLV_K * CLV_MAX_VARIANTS; t += SNT) {
+            flist[p][t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS] = T.feas_list[t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS];
+            if (t < CLV_K) nfeas[p][t] = T.nfeas[t];
+        }
+    }
+    for (int r = threadIdx.x; r < P.K; r += SNT) {
+        nsl[r] = (unsigned char)P.nslices[r];
+        for (int j = 0; j < 8; ++j) kinds[r][j] = P.kinds[r][j];
+    }
+    __syncthreads();
+    const uint32_t K = (uint32_t)P.K;
+    RecP r0 = recp_none(), r1 = recp_none();
+    unsigned long long c_valid = 0, c_sla = 0;
+    for (long long i = a.begin + (long long)blockIdx.x * SNT + threadIdx.x; i < a.end;
+         i += (long long)gridDim.x * SNT) {
+        Draws d;
+        d.h0 = derive_seed2(a.seed, (uint64_t)i);
+        d.j = 0; d.word = 0;
+        double f = 0.0, h = 0.0;
+        bool sla = true;
+        for (int p = 0; p < a.n_pods; ++p) {
+            long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+            unsigned long long m = 0;
+            for (int g = 0; g < a.pods[p].n_gpus; ++g) {
+                const int r = d.bounded(K);
+                const int ns = nsl[r];
+                for (int j = 0; j < ns; ++j) {
+                    const int k = kinds[r][j];
+                    const int v = flist[p][k][d.bounded(nfeas[p][k])];
+                    const int e = v * 5 + k;
+                    S0 += row[p][e].thr; S1 += row[p][e].acc; S2 += row[p][e].en; S3 += row[p][e].idle;
+                    m |= 1ULL << rank[p][e];
+                }
+            }
+            Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[p][63 - __clzll((long long)m)], a.pods[p].ec);
+            const double wt = a.pods[p].weight;
+            if (p == 0) { f = wt * sc.f; h = wt * sc.h; }
+            else { f = f + wt * sc.f; h = h + wt * sc.h; }
+            sla = sla && sc.sla;
+        }
+        Score comb;
+        comb.f = f; comb.h = h; comb.L = 0.0; comb.A = 0.0; comb.E = 0.0; comb.sla = sla;
+        ++c_valid;
+        c_sla += sla;
+        consider(r0, r1, comb, i, CLV_SELECT_BEST_H);
+        const long long o = i - a.begin;
+        if (a.f_out) a.f_out[o] = f;
+        if (a.h_out) a.h_out[o] = h;
+        if (a.sla_out) a.sla_out[o] = sla;
+    }
+    grid_finish<SNT>(r0, r1, c_valid, c_sla, a.sel);
+}
+
+cudaError_t launch_sweep(const SweepArgs &a, int grid, cudaStream_t s) {
+    sweep_kernel<<<grid, SNT, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------- chain / rank winner
+__device__ inline void rec_min_block(clv_record &best) {
+    __shared__ clv_record sm[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int m = 16; m >= 1; m >>= 1) {
+        clv_record o;
+        o.k1 = __shfl_xor_sync(0xFFFFFFFFu, best.k1, m);
+        o.k2 = __shfl_xor_sync(0xFFFFFFFFu, best.k2, m);
+        o.index = __shfl_xor_sync(0xFFFFFFFFu, best.index, m);
+        o.h = __shfl_xor_sync(0xFFFFFFFFu, best.h, m);
+        bool less = o.k1 != best.k1 ? o.k1 < best.k1 : (o.k2 != best.k2 ? o.k2 < best.k2 : o.index < best.index);
+        if (less) best = o;
+    }
+    if (lane == 0) sm[wid] = best;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        clv_record none = {~0ULL, ~0ULL, 0x7FFFFFFFFFFFFFFFLL, 0.0};
+        best = lane < nw ? sm[lane] : none;
+        for (int m = 16; m >= 1; m >>= 1) {
+            clv_record o;
+            o.k1 = __shfl_xor_sync(0xFFFFFFFFu, best.k1, m);
+            o.k2 = __shfl_xor_sync(0xFFFFFFFFu, best.k2, m);
+            o.index = __shfl_xor_sync(0xFFFFFFFFu, best.index, m);
+            o.h = __shfl_xor_sync(0xFFFFFFFFu, best.h, m);
+            bool less = o.k1 != best.k1 ? o.k1 < best.k1 : (o.k2 != best.k2 ? o.k2 < best.k2 : o.index < best.index);
+            if (less) best = o;
+        }
+    }
+}
+
+__global__ void select_chains_kernel(const clv_chain_result *res, int n_chains, long long chain_base,
+                                     clv_record *out) {
+    clv_record best = {~0ULL, ~0ULL, 0x7FFFFFFFFFFFFFFFLL, 0.0};
+    for (int c = threadIdx.x; c < n_chains; c += blockDim.x) {
+        const clv_chain_result &r = res[c];
+        if (r.status < 0) continue;
+        clv_record x;
+        x.k1 = r.sla_met ? 0ULL : 1ULL;
+        x.k2 = okey(r.h);
+        x.index = chain_base + c;
+        x.h = r.h;
+        bool less = x.k1 != best.k1 ? x.k1 < best.k1 : (x.k2 != best.k2 ? x.k2 < best.k2 : x.index < best.index);
+        if (less) best = x;
+    }
+    rec_min_block(best);
+    if (threadIdx.x == 0) *out = best;
+}
+
+cudaError_t launch_select_chains(const clv_chain_result *res, int n_chains, long long chain_base,
+                                 clv_record *out, cudaStream_t s) {
+    select_chains_kernel<<<1, 256, 0, s>>>(res, n_chains, chain_base, out);
+    return cudaGetLastError();
+}
+
+__global__ void reduce_records_kernel(const clv_record *recs, int count, clv_record *out) {
+    clv_record best = {~0ULL, ~0ULL, 0x7FFFFFFFFFFFFFFFLL, 0.0};
+    for (int c = threadIdx.x; c < count; c += blockDim.x) {
+        clv_record x = recs[c];
+        bool less = x.k1 != best.k1 ? x.k1 < best.k1 : (x.k2 != best.k2 ? x.k2 < best.k2 : x.index < best.index);
+        if (less) best = x;
+    }
+    rec_min_block(best);
+    if (threadIdx.x == 0) *out = best;
+}
+
+cudaError_t launch_reduce_records(const clv_record *recs, int count, clv_record *out, cudaStream_t s) {
+    reduce_records_kernel<<<1, 256, 0, s>>>(recs, count, out);
+    return cudaGetLastError();
+}
+
+}  // namespace clv

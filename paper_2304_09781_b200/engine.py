@@ -1,0 +1,389 @@
+"""CloverEngine: the device-side configuration-search engine (one per GPU).
+
+Thin host orchestration over the C-ABI (include/clover.h).  Device buffers are
+torch tensors (plumbing only); every candidate is decoded, scored and selected
+by the sm_100a kernels in csrc/.  Nothing here evaluates a candidate on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .core import SLICE_ORDER, ObjectiveParams, SliceType
+from .errors import CarbonSchedError, DeviceError, InfeasibleGraphError
+from .graph import ConfigGraph
+from .mig import DEFAULT_TOPOLOGY, FleetConfig, MigTopology
+from .objective import AnnealParams, Scenario
+from .profiles import ProfileTable, ScoringTables
+
+SELECT = {"best_h": 0, "oracle": 1}
+
+
+def _torch():
+    try:
+        import torch
+    except ImportError as exc:  # pragma: no cover
+        raise DeviceError("torch is required for device buffers") from exc
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible; the Clover engine has no CPU fallback")
+    return torch
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def eval_params(s: Scenario) -> N.EvalParams:
+    o = s.obj
+    return N.EvalParams(float(s.arrival_rps), float(s.ci), float(o.carbon_weight), float(o.base_accuracy),
+                        float(o.base_carbon_g), float(o.latency_slo_ms), float(s.rho_sat),
+                        1 if s.strict_eq6 else 0, int(s.n_gpus))
+
+
+@dataclass
+class AnnealBatch:
+    """Device-resident results of one clv_anneal launch (torch tensors on the GPU)."""
+
+    results: object        # uint8 [n_chains * 72] viewed through CHAIN_DTYPE on host
+    best_w: object         # uint16 [n_chains, E]
+    final_w: object        # uint16 [n_chains, E]
+    log: object            # optional uint8 [n_chains * max_steps * 56]
+    n_chains: int
+    chain_base: int
+    max_steps: int
+
+    def host(self) -> dict:
+        res = np.frombuffer(self.results.cpu().numpy().tobytes(), dtype=CHAIN_DTYPE)
+        out = {"results": res, "best_w": self.best_w.cpu().numpy(), "final_w": self.final_w.cpu().numpy()}
+        if self.log is not None:
+            out["log"] = np.frombuffer(self.log.cpu().numpy().tobytes(), dtype=LOG_DTYPE).reshape(
+                self.n_chains, self.max_steps)
+        return out
+
+
+CHAIN_DTYPE = np.dtype([("f", "<f8"), ("h", "<f8"), ("p95_ms", "<f8"), ("accuracy", "<f8"),
+                        ("energy_wh", "<f8"), ("sla_met", "<i4"), ("status", "<i4"), ("steps", "<i4"),
+                        ("best_step", "<i4"), ("best_index", "<i8"), ("evals", "<i8")])
+LOG_DTYPE = np.dtype([("temp", "<f8"), ("f", "<f8"), ("h", "<f8"), ("p95_ms", "<f8"), ("iter", "<i4"),
+                      ("ged_from_center", "<i4"), ("sla_met", "<i4"), ("accepted", "<i4"),
+                      ("new_best", "<i4"), ("pad", "<i4")])
+RECORD_DTYPE = np.dtype([("k1", "<u8"), ("k2", "<u8"), ("index", "<i8"), ("h", "<f8")])
+assert CHAIN_DTYPE.itemsize == ctypes.sizeof(N.ChainResult) == 72
+assert LOG_DTYPE.itemsize == ctypes.sizeof(N.LogRow) == 56
+assert RECORD_DTYPE.itemsize == ctypes.sizeof(N.Record) == 32
+
+
+class CloverEngine:
+    """One native context on one CUDA device.
+
+    Profiles are registered as families (up to 8); feasibility tables cover
+    fleets of up to ``n_max`` GPUs (clv_build_feasibility, K6).
+    """
+
+    def __init__(self, topology: MigTopology = DEFAULT_TOPOLOGY, device: Optional[int] = None,
+                 n_max: int = 0):
+        torch = _torch()
+        self.torch = torch
+        self.lib = N.load()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        ctx = ctypes.c_void_p()
+        rc = self.lib.clv_create(self.device, ctypes.byref(ctx))
+        if rc != 0:
+            raise DeviceError("clv_create failed with status %d" % rc)
+        self.ctx = ctx
+        self.topology = topology
+        ids = np.array(topology.config_ids, dtype=np.int32)
+        counts = np.ascontiguousarray(np.array(topology.config_vectors, dtype=np.int32))
+        mem = np.array([topology.slice_memory(s) for s in SLICE_ORDER], dtype=np.float64)
+        self._check(self.lib.clv_set_topology(ctx, len(ids), ids.ctypes.data, counts.ctypes.data, mem.ctypes.data))
+        self._families: dict[str, tuple[int, ProfileTable, ScoringTables]] = {}
+        self.n_max = 0
+        if n_max:
+            self.build_feasibility(n_max)
+
+    # -- lifecycle -----------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "ctx", None):
+            self.lib.clv_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int) -> None:
+        N.check(rc, self.ctx)
+
+    def _stream(self, stream=None) -> int:
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        return s.cuda_stream
+
+    # -- tables ----------------------------------------------------------------
+    def add_profile(self, profile: ProfileTable) -> int:
+        if profile.name in self._families:
+            return self._families[profile.name][0]
+        fam = len(self._families)
+        if fam >= 8:
+            raise CarbonSchedError("at most 8 profile families per engine")
+        if profile.topology is not self.topology and profile.topology.to_json_dict() != self.topology.to_json_dict():
+            raise CarbonSchedError("profile was built for a different topology")
+        t = profile.scoring_tables()
+        arr = lambda x, dt: np.ascontiguousarray(np.asarray(x, dtype=dt))
+        thr, acc, en, idle = arr(t.thr_q, np.int64), arr(t.acc_q, np.int64), arr(t.en_q, np.int64), arr(t.idle_q, np.int64)
+        lat, mem = arr(t.lat95, np.float64), arr(t.mem_ok, np.uint8)
+        self._check(self.lib.clv_set_profile(self.ctx, fam, t.variant_count, thr.ctypes.data, acc.ctypes.data,
+                                             en.ctypes.data, idle.ctypes.data, lat.ctypes.data, mem.ctypes.data,
+                                             t.kt, t.ke, t.ki))
+        self._families[profile.name] = (fam, profile, t)
+        return fam
+
+    def family(self, profile: ProfileTable) -> int:
+        return self.add_profile(profile)
+
+    def build_feasibility(self, n_max: int) -> None:
+        self._check(self.lib.clv_build_feasibility(self.ctx, int(n_max), self._stream()))
+        self.n_max = int(n_max)
+
+    def ensure_feasibility(self, n: int) -> None:
+        if n > self.n_max:
+            self.build_feasibility(max(n, self.n_max))
+
+    @property
+    def feasibility_bytes(self) -> int:
+        return int(self.lib.clv_feasibility_bytes(self.ctx))
+
+    # -- feasibility / realize ---------------------------------------------------
+    def feasible(self, vecs, n: int):
+        torch = self.torch
+        self.ensure_feasibility(n)
+        v = torch.as_tensor(np.asarray(vecs, dtype=np.int32).reshape(-1, 5), device="cuda:%d" % self.device)
+        out = torch.empty(v.shape[0], dtype=torch.uint8, device=v.device)
+        self._check(self.lib.clv_feasible(self.ctx, int(n), v.data_ptr(), v.shape[0], out.data_ptr(), self._stream()))
+        return out
+
+    def partition(self, vec: Sequence[int], n: int) -> tuple[int, ...]:
+        """Canonical config ids (ascending) realizing a slice-count vector (mig.py:172-177)."""
+        self.ensure_feasibility(n)
+        v = np.ascontiguousarray(np.asarray(vec, dtype=np.int32))
+        parts = np.zeros(max(n, 1), dtype=np.int32)
+        self._check(self.lib.clv_realize(self.ctx, int(n), v.ctypes.data, parts.ctypes.data, self._stream()))
+        return tuple(int(x) for x in parts[:n])
+
+    def realize(self, g: ConfigGraph, n: int) -> FleetConfig:
+        """realize(g, n): canonical partitions, then variants per slice in
+        canonical order, smallest variant first."""
+        parts = self.partition(g.slice_vector(), n)
+        left = list(g.weights)
+        V = g.variant_count
+        assign = []
+        for cid in parts:
+            for s in self.topology.config_slices(cid):
+                k = s.index
+                for v in range(V):
+                    if left[v * 5 + k] > 0:
+                        left[v * 5 + k] -= 1
+                        assign.append(v + 1)
+                        break
+                else:  # pragma: no cover - realize is exact
+                    raise InfeasibleGraphError("realize lost a slice")
+        return FleetConfig(parts, assign, self.topology)
+
+    # -- scoring -------------------------------------------------------------------
+    def score_graphs(self, W, profile: ProfileTable, scenario: Scenario, select: str = "best_h",
+                     outputs: bool = True, index_base: int = 0, stream=None) -> tuple[dict, dict]:
+        torch = self.torch
+        fam = self.add_profile(profile)
+        self.ensure_feasibility(scenario.n_gpus)
+        W = torch.as_tensor(W).to(device="cuda:%d" % self.device, dtype=torch.uint16).contiguous()
+        count = W.shape[0]
+        outs = {}
+        if outputs:
+            outs = {"f": torch.empty(count, dtype=torch.float64, device=W.device),
+                    "h": torch.empty(count, dtype=torch.float64, device=W.device),
+                    "p95": torch.empty(count, dtype=torch.float64, device=W.device),
+                    "sla": torch.empty(count, dtype=torch.uint8, device=W.device),
+                    "feasible": torch.empty(count, dtype=torch.uint8, device=W.device)}
+        best = N.Best()
+        p = eval_params(scenario)
+        self._check(self.lib.clv_score_graphs(
+            self.ctx, fam, W.data_ptr(), count, index_base, ctypes.byref(p), SELECT[select],
+            _ptr(outs.get("f")), _ptr(outs.get("h")), _ptr(outs.get("sla")), _ptr(outs.get("feasible")),
+            _ptr(outs.get("p95")), ctypes.byref(best), self._stream(stream)))
+        return best.as_dict(), outs
+
+    def score_fleets(self, fleets: Sequence[FleetConfig], profile: ProfileTable, scenario: Scenario,
+                     select: str = "best_h", outputs: bool = True) -> tuple[dict, dict]:
+        """Score FleetConfigs (x^p, x^v) of one fleet size on the device (K1 decode)."""
+        n = fleets[0].n_gpus
+        xp = np.array([f.partitions for f in fleets], dtype=np.uint8)
+        xv = np.concatenate([np.array(f.assignments, dtype=np.int64) for f in fleets]).clip(0, 255).astype(np.uint8)
+        off = np.zeros(len(fleets) + 1, dtype=np.int64)
+        off[1:] = np.cumsum([len(f.assignments) for f in fleets])
+        return self.score_x(xp, xv, off, n, profile, scenario, select, outputs)
+
+    def score_x(self, xp, xv, offsets, n: int, profile: ProfileTable, scenario: Scenario,
+                select: str = "best_h", outputs: bool = True, index_base: int = 0, stream=None):
+        torch = self.torch
+        fam = self.add_profile(profile)
+        dev = "cuda:%d" % self.device
+        xp = torch.as_tensor(xp).to(device=dev, dtype=torch.uint8).contiguous()
+        xv = torch.as_tensor(xv).to(device=dev, dtype=torch.uint8).contiguous()
+        offsets = torch.as_tensor(offsets).to(device=dev, dtype=torch.int64).contiguous()
+        count = offsets.shape[0] - 1
+        outs = {}
+        if outputs:
+            outs = {"f": torch.empty(count, dtype=torch.float64, device=dev),
+                    "h": torch.empty(count, dtype=torch.float64, device=dev),
+                    "sla": torch.empty(count, dtype=torch.uint8, device=dev)}
+        best = N.Best()
+        p = eval_params(scenario)
+        self._check(self.lib.clv_score_x(self.ctx, fam, int(n), xp.data_ptr(), xv.data_ptr(), offsets.data_ptr(),
+                                         count, index_base, ctypes.byref(p), SELECT[select],
+                                         _ptr(outs.get("f")), _ptr(outs.get("h")), _ptr(outs.get("sla")),
+                                         ctypes.byref(best), self._stream(stream)))
+        return best.as_dict(), outs
+
+    def calibrate(self, profile: ProfileTable, n: int, ci: float, lam: float = 0.5, utilization: float = 0.7,
+                  ci_base: Optional[float] = None, strict: bool = False, pue: float = 1.5) -> Scenario:
+        """R = utilization x BASE capacity; A_base, C_base, L_tail from scoring BASE on the device
+        (C_base without PUE)."""
+        V = profile.variant_count
+        R = utilization * n * (1000.0 / profile.mean_service_ms(V, SliceType.S7G))
+        probe = Scenario(n, R, float(ci), ObjectiveParams(1.0, 1.0, 1.0, lam, pue), strict)
+        w = np.zeros((1, V * 5), dtype=np.uint16)
+        w[0, (V - 1) * 5] = n
+        best, outs = self.score_graphs(w, profile, probe, outputs=False)
+        if not best["found"]:
+            raise InfeasibleGraphError("BASE is not realizable")
+        cb = float(ci if ci_base is None else ci_base)
+        obj = ObjectiveParams(best["accuracy"], best["energy_wh"] / 1000.0 * cb, best["p95_ms"], lam, pue)
+        return Scenario(n, R, float(ci), obj, strict)
+
+    # -- ORACLE (exhaustive standardized search) ----------------------------------------
+    def oracle_size(self, profile: ProfileTable) -> int:
+        fam = self.add_profile(profile)
+        tot = ctypes.c_int64()
+        self._check(self.lib.clv_oracle_size(self.ctx, fam, ctypes.byref(tot)))
+        return tot.value
+
+    def oracle_decode(self, profile: ProfileTable, index: int) -> tuple[int, tuple[int, ...]]:
+        fam = self.add_profile(profile)
+        cid, ns = ctypes.c_int32(), ctypes.c_int32()
+        buf = (ctypes.c_int32 * 8)()
+        self._check(self.lib.clv_oracle_decode(self.ctx, fam, int(index), ctypes.byref(cid), buf, ctypes.byref(ns)))
+        return cid.value, tuple(buf[i] for i in range(ns.value))
+
+    def oracle_search(self, profile: ProfileTable, scenario: Scenario, begin: int = 0,
+                      end: Optional[int] = None, stream=None) -> dict:
+        fam = self.add_profile(profile)
+        best = N.Best()
+        tot = ctypes.c_int64()
+        p = eval_params(scenario)
+        self._check(self.lib.clv_oracle_search(self.ctx, fam, scenario.n_gpus, int(begin),
+                                               -1 if end is None else int(end), ctypes.byref(p),
+                                               ctypes.byref(best), ctypes.byref(tot), self._stream(stream)))
+        out = best.as_dict()
+        out["total"] = tot.value
+        return out
+
+    # -- annealing chains -------------------------------------------------------------
+    def anneal(self, starts, profile: ProfileTable, scenarios, ap: AnnealParams, seed: int,
+               n: Optional[int] = None, chain_base: int = 0, cluster: int = 8, log: bool = False,
+               stream=None, out: Optional[AnnealBatch] = None) -> AnnealBatch:
+        """Run ``len(starts)`` independent chains to termination in one launch (K3+K4+K5)."""
+        torch = self.torch
+        fam = self.add_profile(profile)
+        dev = "cuda:%d" % self.device
+        if isinstance(starts, (list, tuple)) and starts and isinstance(starts[0], ConfigGraph):
+            starts = np.array([g.weights for g in starts], dtype=np.uint16)
+        W0 = torch.as_tensor(starts).to(device=dev, dtype=torch.uint16).contiguous()
+        n_chains = W0.shape[0]
+        if isinstance(scenarios, Scenario):
+            scenarios = [scenarios]
+        n = scenarios[0].n_gpus if n is None else int(n)
+        self.ensure_feasibility(n)
+        E = profile.variant_count * 5
+        if W0.shape[1] != E:
+            raise CarbonSchedError("start graphs need %d edge weights" % E)
+        params = (N.EvalParams * len(scenarios))(*[eval_params(s) for s in scenarios])
+        apc = N.AnnealParamsC(ap.t_init, ap.cooling_step, ap.t_floor, ap.stall_limit, ap.step_limit(),
+                              1 if ap.proposal == "uniform" else 0, 1 if ap.evaluate == "proposal" else 0)
+        steps = ap.step_limit()
+        if out is None or out.n_chains != n_chains or (log and out.log is None):
+            out = AnnealBatch(torch.empty(n_chains * 72, dtype=torch.uint8, device=dev),
+                              torch.empty((n_chains, E), dtype=torch.uint16, device=dev),
+                              torch.empty((n_chains, E), dtype=torch.uint16, device=dev),
+                              torch.zeros(max(1, n_chains * steps * 56), dtype=torch.uint8, device=dev) if log else None,
+                              n_chains, chain_base, steps)
+        out.chain_base = chain_base
+        self._check(self.lib.clv_anneal(self.ctx, fam, n, n_chains, int(chain_base), W0.data_ptr(), params,
+                                        len(scenarios), ctypes.byref(apc), int(seed) & ((1 << 64) - 1),
+                                        int(cluster), out.results.data_ptr(), out.best_w.data_ptr(),
+                                        out.final_w.data_ptr(), _ptr(out.log), self._stream(stream)))
+        return out
+
+    def select_chains(self, batch: AnnealBatch, record=None, stream=None):
+        """Winner of a batch of chains as a 32-byte device record (SLA desc, h asc, chain asc)."""
+        torch = self.torch
+        if record is None:
+            record = torch.empty(32, dtype=torch.uint8, device="cuda:%d" % self.device)
+        self._check(self.lib.clv_select_chains(self.ctx, batch.results.data_ptr(), batch.n_chains,
+                                               batch.chain_base, record.data_ptr(), self._stream(stream)))
+        return record
+
+    def reduce_records(self, records, out=None, stream=None):
+        torch = self.torch
+        if out is None:
+            out = torch.empty(32, dtype=torch.uint8, device=records.device)
+        count = records.numel() // 32
+        self._check(self.lib.clv_reduce_records(self.ctx, records.data_ptr(), count, out.data_ptr(),
+                                                self._stream(stream)))
+        return out
+
+    # -- counter-RNG sweep ------------------------------------------------------------
+    def _pods(self, pods):
+        arr = (N.Pod * len(pods))()
+        for i, (profile, scenario, n_gpus, weight) in enumerate(pods):
+            arr[i] = N.Pod(self.add_profile(profile), int(n_gpus), float(weight), eval_params(scenario))
+        return arr
+
+    def sweep(self, pods, begin: int, end: int, seed: int, outputs: bool = False, stream=None):
+        """Score x-space candidates [begin, end) drawn from the counter RNG."""
+        torch = self.torch
+        arr = self._pods(pods)
+        dev = "cuda:%d" % self.device
+        count = int(end) - int(begin)
+        outs = {}
+        if outputs:
+            outs = {"f": torch.empty(count, dtype=torch.float64, device=dev),
+                    "h": torch.empty(count, dtype=torch.float64, device=dev),
+                    "sla": torch.empty(count, dtype=torch.uint8, device=dev)}
+        best = N.Best()
+        self._check(self.lib.clv_sweep(self.ctx, len(pods), arr, int(begin), int(end), int(seed) & ((1 << 64) - 1),
+                                       _ptr(outs.get("f")), _ptr(outs.get("h")), _ptr(outs.get("sla")),
+                                       ctypes.byref(best), self._stream(stream)))
+        return best.as_dict(), outs
+
+    def sweep_decode(self, pods, seed: int, index: int) -> list[FleetConfig]:
+        arr = self._pods(pods)
+        n_total = sum(int(p[2]) for p in pods)
+        parts = np.zeros(n_total, dtype=np.int32)
+        assigns = np.zeros(7 * n_total, dtype=np.int32)
+        na = ctypes.c_int32()
+        self._check(self.lib.clv_sweep_decode(self.ctx, len(pods), arr, int(seed) & ((1 << 64) - 1), int(index),
+                                              parts.ctypes.data, assigns.ctypes.data, ctypes.byref(na)))
+        out, g0, s0 = [], 0, 0
+        for profile, _sc, n_gpus, _w in pods:
+            p = parts[g0:g0 + n_gpus]
+            m = sum(len(self.topology.config_slices(int(c))) for c in p)
+            out.append(FleetConfig(p.tolist(), assigns[s0:s0 + m].tolist(), self.topology))
+            g0 += n_gpus
+            s0 += m
+        return out
