@@ -111,7 +111,7 @@ typedef struct clv_chain_result {
 /* One row of the optional per-step log (SPEC:487 schema). */
 typedef struct clv_log_row {
     double temp, f, h, p95_ms;
-    int32_t iter, ged_from_center, sla_met, accepted, new_best, pad;
+    int32_t iter, ged_from_center, sla_met, accepted, new_best, n_neighbours;
 } clv_log_row;
 
 /* 32-byte winner record exchanged between ranks (one per GPU per round). */

@@ -79,7 +79,7 @@ def anneal_chain(w0, n, tables, scenario, ap, seed, chain, feas, log=False) -> C
         hp, hc = prop["h"], cur["h"]
         accept = hp <= hc or u < exp_clv(-(hp - hc) / T)
         if log:
-            rows.append(dict(iter=k, temp=T, ged_from_center=2 * int(nb.kind[p]), f=prop["f"],
+            rows.append(dict(iter=k, temp=T, ged_from_center=2 * int(nb.kind[p]), n_neighbours=len(nb), f=prop["f"],
                              h=prop["h"], p95_ms=prop["L"], sla_met=prop["sla"],
                              accepted=bool(accept), new_best=bool(new_best)))
         if accept:

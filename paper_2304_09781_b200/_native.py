@@ -45,7 +45,7 @@ class ChainResult(ctypes.Structure):
 class LogRow(ctypes.Structure):
     _fields_ = [("temp", c_f64), ("f", c_f64), ("h", c_f64), ("p95_ms", c_f64), ("iter", c_i32),
                 ("ged_from_center", c_i32), ("sla_met", c_i32), ("accepted", c_i32),
-                ("new_best", c_i32), ("pad", c_i32)]
+                ("new_best", c_i32), ("n_neighbours", c_i32)]
 
 
 class Record(ctypes.Structure):

@@ -129,17 +129,46 @@ __device__ inline void apply_move(AnnealSmem &s, uint32_t mv) {
 // Rebuild the present-edge list, the removal-pair list and the feasibility
 // bytes of all 25 single / 625 double slice deltas (all threads).
 __device__ inline void prepare_step(AnnealSmem &s, int E, int n, const FeasView &F) {
-    if (threadIdx.x == 0) { s.nPE = 0; s.nRP = 0; }
-    __syncthreads();
-    int NP = E * (E + 1) / 2;
-    for (int p = threadIdx.x; p < NP; p += ANT) {
-        int x = s.pair_tab[p] & 0xFF, y = s.pair_tab[p] >> 8;
-        int wx = s.w[x], wy = s.w[y];
-        bool ok = (x == y) ? (wx >= 2) : (wx > 0 && wy > 0);
-        if (ok) s.rp[atomicAdd(&s.nRP, 1)] = (unsigned short)(x | (y << 8));
+    // Ordered (deterministic) compaction: every CTA of the cluster must build
+    // identical lists, because the cluster partitions the move space by list
+    // position.
+    __shared__ int warp_off[NWARP + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int NP = E * (E + 1) / 2;
+    int base = 0;
+    for (int p0 = 0; p0 < NP; p0 += ANT) {
+        const int p = p0 + threadIdx.x;
+        bool ok = false;
+        int x = 0, y = 0;
+        if (p < NP) {
+            x = s.pair_tab[p] & 0xFF; y = s.pair_tab[p] >> 8;
+            const int wx = s.w[x], wy = s.w[y];
+            ok = (x == y) ? (wx >= 2) : (wx > 0 && wy > 0);
+        }
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
+        if (lane == 0) warp_off[wid] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int q = 0; q < NWARP; ++q) { int c = warp_off[q]; warp_off[q] = acc; acc += c; }
+            warp_off[NWARP] = acc;
+        }
+        __syncthreads();
+        if (ok) s.rp[base + warp_off[wid] + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)(x | (y << 8));
+        base += warp_off[NWARP];
+        __syncthreads();
     }
-    for (int e = threadIdx.x; e < E; e += ANT)
-        if (s.w[e] > 0) s.pe[atomicAdd(&s.nPE, 1)] = (unsigned char)e;
+    if (wid == 0) {
+        int cnt = 0;
+        for (int e0 = 0; e0 < E; e0 += 32) {
+            const int e = e0 + lane;
+            const bool ok = e < E && s.w[e] > 0;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
+            if (ok) s.pe[cnt + __popc(bal & ((1u << lane) - 1u))] = (unsigned char)e;
+            cnt += __popc(bal);
+        }
+        if (lane == 0) { s.nPE = cnt; s.nRP = base; }
+    }
     for (int t = threadIdx.x; t < 650; t += ANT) {
         int v[CLV_K];
 #pragma unroll
@@ -391,7 +420,7 @@ __global__ void __launch_bounds__(ANT) anneal_kernel(const __grid_constant__ Ann
                     clv_log_row row;
                     row.temp = Tk; row.f = fp; row.h = hp; row.p95_ms = Lp;
                     row.iter = k; row.ged_from_center = (r2 == 0xFF) ? 2 : 4; row.sla_met = slap;
-                    row.accepted = acc; row.new_best = nb; row.pad = 0;
+                    row.accepted = acc; row.new_best = nb; row.n_neighbours = (int)total;
                     args.log[(size_t)chain * args.max_steps + k] = row;
                 }
                 if (acc) {

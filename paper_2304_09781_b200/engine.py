@@ -71,7 +71,7 @@ CHAIN_DTYPE = np.dtype([("f", "<f8"), ("h", "<f8"), ("p95_ms", "<f8"), ("accurac
                         ("best_step", "<i4"), ("best_index", "<i8"), ("evals", "<i8")])
 LOG_DTYPE = np.dtype([("temp", "<f8"), ("f", "<f8"), ("h", "<f8"), ("p95_ms", "<f8"), ("iter", "<i4"),
                       ("ged_from_center", "<i4"), ("sla_met", "<i4"), ("accepted", "<i4"),
-                      ("new_best", "<i4"), ("pad", "<i4")])
+                      ("new_best", "<i4"), ("n_neighbours", "<i4")])
 RECORD_DTYPE = np.dtype([("k1", "<u8"), ("k2", "<u8"), ("index", "<i8"), ("h", "<f8")])
 assert CHAIN_DTYPE.itemsize == ctypes.sizeof(N.ChainResult) == 72
 assert LOG_DTYPE.itemsize == ctypes.sizeof(N.LogRow) == 56
