@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Benchmark: candidate configurations scored per second by the Clover re-plan.
+
+Default workload (BASELINE.json configs[2], the multi-GPU one; per-GPU share at
+N GPUs, weak scaling): a 64-GPU fleet, EfficientNet B1-B7 catalog (V=7),
+lambda=0.5, 128 independent annealing chains per B200 (1024 on 8), each from a
+random realizable start, full GED<=4 neighbourhood scored every step, run to
+termination (stall 5 / 64 steps).  One bench step = one complete re-plan of all
+chains (so ms_per_step is the per-re-plan time-to-solution) followed by the
+per-round winner exchange (NCCL all_gather of 32-byte records when N > 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl clover|reference]
+
+The reference arm (--impl reference) runs the CPU oracle port of the same
+algorithm (oracle/, a restatement of the SPEC; the reference ships no optimiser
+code) on all host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate configs scored/sec (objective+SLA) at 1/2/4/8 B200; re-plan time-to-solution"
+UNIT = "candidates/s"
+N_FLEET = 64
+CHAINS_PER_GPU = 128
+FAMILY = "efficientnet"
+LAMBDA = 0.5
+CI = 350.0
+SEED = 230409781
+FLOPS_PER_CANDIDATE = 24          # fp64 ops of the scoring epilogue
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="clover", choices=["clover", "reference"])
+    ap.add_argument("--chains", type=int, default=CHAINS_PER_GPU)
+    ap.add_argument("--cluster", type=int, default=8)
+    ap.add_argument("--max-steps", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def anneal_params(max_steps):
+    from paper_2304_09781_b200.objective import AnnealParams
+    return AnnealParams(max_steps=max_steps, stall_limit=5, proposal="best", evaluate="all")
+
+
+def make_starts(engine, profile, seed, first, count):
+    from paper_2304_09781_b200.search import random_fleets
+    from paper_2304_09781_b200.graph import build_graph
+    fleets = random_fleets(engine, profile, N_FLEET, seed, count, first)
+    return np.array([build_graph(f, profile).weights for f in fleets], dtype=np.uint16)
+
+
+class ClockSampler:
+    def __init__(self, index, path):
+        self.path = path
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def fp64_peak_tflops():
+    """Measured FP64 FMA peak of this B200 (tools/microbench.cu), TFLOP/s."""
+    try:
+        import ctypes
+        lib = ctypes.CDLL(os.path.join(ROOT, "tools", "libclv_microbench.so"))
+        lib.clv_mb_fp64_tflops.restype = ctypes.c_double
+        lib.clv_mb_fp64_tflops.argtypes = [ctypes.c_int]
+        return float(lib.clv_mb_fp64_tflops(0)), "measured (tools/microbench.cu DFMA loop)"
+    except Exception as exc:  # pragma: no cover
+        return None, "unavailable: %s" % exc
+
+
+# ------------------------------------------------------------------- CPU legs
+def _cpu_chain(args):
+    (w0, chain, seed, max_steps) = args
+    from oracle.anneal import anneal_chain
+    t0 = time.perf_counter()
+    out = anneal_chain(w0, N_FLEET, _CPU["T"], _CPU["sc"], anneal_params(max_steps), seed, chain, _CPU["feas"])
+    return out.evals, time.perf_counter() - t0
+
+
+_CPU = {}
+
+
+def _cpu_setup(scenario_tuple):
+    from oracle.tables import OracleTables
+    from oracle.feasibility import FeasOracle
+    from oracle.evaluator import calibrate
+    from paper_2304_09781_b200.profiles import synthetic_profile
+    from paper_2304_09781_b200.mig import DEFAULT_TOPOLOGY
+    prof = synthetic_profile(FAMILY)
+    T = OracleTables.from_profile(prof)
+    _CPU["T"] = T
+    _CPU["sc"] = calibrate(prof, T, N_FLEET, CI, LAMBDA)
+    _CPU["feas"] = FeasOracle(DEFAULT_TOPOLOGY, N_FLEET)
+
+
+def cpu_baseline(starts, seed, max_steps, seconds):
+    """Oracle port on one host core over a bounded sample of the same chains."""
+    _cpu_setup(None)
+    evals, spent, chains = 0, 0.0, 0
+    for c in range(len(starts)):
+        e, t = _cpu_chain((starts[c].astype(np.int64), c, seed, max_steps))
+        evals += e
+        spent += t
+        chains += 1
+        if spent >= seconds:
+            break
+    return {"value": evals / spent, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": "%d of the step-0 chains (n=%d, V=7) annealed to termination by oracle/anneal.py, "
+                      "%d candidates in %.1f s" % (chains, N_FLEET, evals, spent)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    from paper_2304_09781_b200.profiles import synthetic_profile
+    cores = len(os.sched_getaffinity(0))
+    _cpu_setup(None)
+    prof = synthetic_profile(FAMILY)
+    starts = _reference_starts(prof, (args.warmup + args.steps) * cores)
+    ctx = mp.get_context("fork")
+    total_evals, total_time = 0, 0.0
+    with ctx.Pool(cores) as pool:
+        for step in range(args.warmup + args.steps):
+            batch = [(starts[step * cores + i].astype(np.int64), step * cores + i, SEED + step, args.max_steps)
+                     for i in range(cores)]
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_chain, batch)
+            dt = time.perf_counter() - t0
+            if step >= args.warmup:
+                total_evals += sum(r[0] for r in res)
+                total_time += dt
+    value = total_evals / total_time
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * total_time / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": _config(args, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": "%d chains per step (one per core), n=%d, V=7, oracle/anneal.py" % (cores, N_FLEET)},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _reference_starts(prof, count):
+    """Same counter-RNG draws as the GPU arm, decoded by the oracle (no GPU here)."""
+    from oracle.search import Pod, draw_candidate, fleet_graph
+    from paper_2304_09781_b200.mig import DEFAULT_TOPOLOGY
+    T = _CPU["T"]
+    out = []
+    for i in range(count):
+        (parts, assign), = draw_candidate(SEED, i, [Pod(T, None, N_FLEET, 1.0)], DEFAULT_TOPOLOGY)
+        out.append(fleet_graph(parts, assign, DEFAULT_TOPOLOGY, T))
+    return np.array(out, dtype=np.uint16)
+
+
+def _config(args, world, cores_chains=None):
+    return {"workload": "c2: n=%d-GPU fleet, %s B1-B7 (V=7), lambda=%.1f, ci=%.0f gCO2/kWh, %d annealing chains "
+                        "per B200 from random realizable starts, full GED<=4 neighbourhood scored per step, "
+                        "run to termination (stall 5, <=%d steps); one step = one re-plan of all chains"
+                        % (N_FLEET, FAMILY, LAMBDA, CI, args.chains if cores_chains is None else cores_chains,
+                           args.max_steps),
+            "fleet_gpus": N_FLEET, "variants": 7, "chains_per_gpu": args.chains if cores_chains is None else cores_chains,
+            "chains_total": (args.chains * world) if cores_chains is None else cores_chains,
+            "proposal": "best-h neighbour", "parallelism": "chains sharded across %d GPU(s), dp%d" % (world, world),
+            "l2": "flushed between steps (256 MiB write outside the timed events)"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2304_09781_b200.engine import CloverEngine, RECORD_DTYPE
+    from paper_2304_09781_b200.profiles import synthetic_profile
+    from paper_2304_09781_b200.search import anneal_chains, exchange_record
+
+    prof = synthetic_profile(FAMILY)
+    eng = CloverEngine(device=local, n_max=N_FLEET)
+    sc = eng.calibrate(prof, N_FLEET, CI, LAMBDA)
+    ap = anneal_params(args.max_steps)
+    C = args.chains
+    total_steps = args.warmup + args.steps
+    base = rank * C
+    # chains of step s, rank r are candidates [s*C*world + r*C, ...) of the counter-RNG stream
+    starts = [make_starts(eng, prof, SEED, s * C * world + base, C) for s in range(total_steps)]
+    starts_dev = [torch.from_numpy(x.view(np.int16)).cuda().view(torch.uint16) for x in starts]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    batches = [None] * total_steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(total_steps)]
+
+    def step(s):
+        e0, e1, e2 = ev[s]
+        e0.record(stream)
+        b = eng.anneal(starts_dev[s], prof, sc, ap, SEED + s, chain_base=base, cluster=args.cluster)
+        e1.record(stream)
+        rec = eng.select_chains(b)
+        exchange_record(eng, rec)
+        e2.record(stream)
+        batches[s] = b
+
+    for s in range(args.warmup):
+        flush.zero_()
+        step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local, os.path.join(ROOT, "gpurun_out", "clocks_rank%d.csv" % rank)) \
+        if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else ClockSampler(local, "/tmp/clv_clocks_%d.csv" % rank)
+    t_wall0 = time.perf_counter()
+    for s in range(args.warmup, total_steps):
+        flush.zero_()
+        step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+    step_ms = [ev[s][0].elapsed_time(ev[s][2]) for s in range(args.warmup, total_steps)]
+    anneal_ms = [ev[s][0].elapsed_time(ev[s][1]) for s in range(args.warmup, total_steps)]
+    evals = sum(int(batches[s].host()["results"]["evals"].sum()) for s in range(args.warmup, total_steps))
+    chain_steps = sum(int(batches[s].host()["results"]["steps"].sum()) for s in range(args.warmup, total_steps))
+    dev_time = sum(step_ms) / 1000.0
+    t = torch.tensor([dev_time, float(evals), sum(anneal_ms) / 1000.0, float(chain_steps)], dtype=torch.float64,
+                     device="cuda")
+    if world > 1:
+        tmax = t.clone(); dist.all_reduce(tmax[0:1], op=dist.ReduceOp.MAX); dist.all_reduce(tmax[2:3], op=dist.ReduceOp.MAX)
+        tsum = t.clone(); dist.all_reduce(tsum[1:2]); dist.all_reduce(tsum[3:4])
+        dev_time, evals_all, anneal_t = tmax[0].item(), tsum[1].item(), tmax[2].item()
+        chain_steps_all = tsum[3].item()
+    else:
+        evals_all, anneal_t, chain_steps_all = float(evals), sum(anneal_ms) / 1000.0, float(chain_steps)
+    value = evals_all / dev_time
+
+    # ---- e2e through the public API (host buffers, copies inside the timed region)
+    e2e_times, e2e_evals = [1e-30], 0
+    for s in (range(args.warmup, total_steps) if not args.no_e2e else []):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = anneal_chains(eng, starts[s], prof, sc, ap, SEED + s, chain_base=base, cluster=args.cluster)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+        e2e_evals += res.evals
+    et = torch.tensor([sum(e2e_times), float(e2e_evals)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        a = et[0:1].clone(); dist.all_reduce(a, op=dist.ReduceOp.MAX)
+        b = et[1:2].clone(); dist.all_reduce(b)
+        e2e_value = b.item() / a.item()
+    else:
+        e2e_value = e2e_evals / sum(e2e_times)
+    E = prof.variant_count * 5
+    h2d = C * E * 2
+    d2h = C * 72 + 2 * C * E * 2 + 32
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = fp64_peak_tflops()
+    per_launch_cand = evals / args.steps
+    avg_anneal_s = sum(anneal_ms) / 1000.0 / args.steps
+    achieved_tflops = per_launch_cand * FLOPS_PER_CANDIDATE / avg_anneal_s / 1e12
+    roof = {"bound": "fp64", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved_tflops / peak) if peak else None, "traffic": None,
+            "kernel": "clv::anneal_kernel", "peak_source": peak_src,
+            "algorithmic": "%d fp64 ops per scored candidate (epilogue) x %.0f candidates per launch"
+                           % (FLOPS_PER_CANDIDATE, per_launch_cand),
+            "anneal_share_of_step": sum(anneal_ms) / sum(step_ms)}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(starts[args.warmup], SEED + args.warmup, args.max_steps, args.cpu_seconds)
+    launches_per_step = 2 + (1 if world > 1 else 0)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * dev_time / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config(args, world), "clocks": clk,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches_per_step * args.steps, "roofline": roof, "cpu_baseline": cpu,
+            "replan_tts_ms": 1000.0 * dev_time / args.steps,
+            "chain_steps_per_replan": chain_steps_all / args.steps,
+            "wall_s_timed_region": t_wall}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,251 @@
+"""Optimiser entry points with the reference's signatures.
+
+``anneal`` / ``oracle_search`` / ``blover_search`` / ``sample_neighbor`` /
+``realize`` keep the SPEC's argument lists and return types on top of the
+reference data model; ``anneal_chains`` is the batched re-plan (many chains,
+one launch, optional cross-GPU winner exchange) that the benchmark and the
+trace controller drive.  All scoring happens in the CUDA kernels.
+"""
+
+from __future__ import annotations
+
+import math
+import random
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .core import ObjectiveParams, SliceType, derive_seed
+from .engine import CloverEngine, CHAIN_DTYPE, RECORD_DTYPE
+from .errors import CarbonSchedError, InfeasibleGraphError, NoNeighborError
+from .graph import ConfigGraph, build_graph
+from .mig import FleetConfig
+from .objective import AnnealParams, Scenario, strict_eq6_default
+from .profiles import ProfileTable
+
+_ENGINES: dict = {}
+
+
+def default_engine(topology=None) -> CloverEngine:
+    """Process-wide engine on the current CUDA device (created lazily)."""
+    import torch
+    from .mig import DEFAULT_TOPOLOGY
+    topo = topology or DEFAULT_TOPOLOGY
+    key = (torch.cuda.current_device(), id(topo))
+    if key not in _ENGINES:
+        _ENGINES[key] = CloverEngine(topo)
+    return _ENGINES[key]
+
+
+@dataclass(frozen=True)
+class Workload:
+    """Poisson request stream; the surrogate uses the rate only."""
+
+    arrival_rate_rps: float
+    duration_s: float = 600.0
+    seed: int = 0
+
+
+@dataclass
+class EvalResult:
+    """SPEC:405-408."""
+
+    graph: ConfigGraph
+    accuracy: float
+    energy_wh_per_request: float
+    p95_ms: float
+    f_value: float
+    h_value: float
+    sla_met: bool
+
+
+def _seed_of(rng) -> int:
+    if rng is None:
+        return 0
+    if isinstance(rng, int):
+        return rng & ((1 << 63) - 1)
+    if hasattr(rng, "seed") and isinstance(getattr(rng, "seed"), int):
+        return rng.seed & ((1 << 63) - 1)
+    if isinstance(rng, (random.Random, np.random.Generator)) or hasattr(rng, "getrandbits"):
+        return int(rng.getrandbits(63)) if hasattr(rng, "getrandbits") else int(rng.integers(0, 1 << 63))
+    raise CarbonSchedError("rng must be an int seed or a seeded random source")
+
+
+def scenario_for(n: int, workload: Workload, ci: float, obj: ObjectiveParams,
+                 strict: Optional[bool] = None) -> Scenario:
+    return Scenario(int(n), float(workload.arrival_rate_rps), float(ci), obj,
+                    strict_eq6_default() if strict is None else bool(strict))
+
+
+def base_config(n: int, catalog: ProfileTable) -> FleetConfig:
+    """BASE: largest variant on every unpartitioned GPU."""
+    V = catalog.variant_count
+    if not catalog.memory_feasible(V, SliceType.S7G):
+        raise CarbonSchedError("largest variant does not fit a 7g slice")
+    return FleetConfig([1] * n, [V] * n, catalog.topology)
+
+
+def co2opt_config(n: int, catalog: ProfileTable) -> FleetConfig:
+    """CO2OPT: configuration 19 with the smallest variant everywhere."""
+    if not catalog.memory_feasible(1, SliceType.S1G):
+        raise CarbonSchedError("smallest variant does not fit a 1g slice")
+    topo = catalog.topology
+    cid = max(topo.config_ids, key=lambda c: (len(topo.config_slices(c)), c))
+    return FleetConfig([cid] * n, [1] * (len(topo.config_slices(cid)) * n), topo)
+
+
+def realize(g: ConfigGraph, n: int, engine: Optional[CloverEngine] = None) -> FleetConfig:
+    """SPEC:206-214 (canonical partition via the device feasibility tables)."""
+    return (engine or default_engine()).realize(g, n)
+
+
+def _result_from_chain(row, graph: ConfigGraph) -> EvalResult:
+    return EvalResult(graph, float(row["accuracy"]), float(row["energy_wh"]), float(row["p95_ms"]),
+                      float(row["f"]), float(row["h"]), bool(row["sla_met"]))
+
+
+@dataclass
+class ChainsResult:
+    best: EvalResult
+    best_chain: int
+    results: np.ndarray          # CHAIN_DTYPE per chain
+    best_w: np.ndarray           # [chains, E]
+    final_w: np.ndarray
+    evals: int                   # candidates scored by all chains of this rank
+    record: np.ndarray = field(default=None)   # winner record (global when exchanged)
+    log: Optional[np.ndarray] = None
+
+
+def exchange_record(engine: CloverEngine, record, group=None):
+    """All-gather the 32-byte winner records of all ranks and reduce them in the same
+    fixed order everywhere: one tiny NCCL collective per round."""
+    import torch.distributed as dist
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        return record
+    world = dist.get_world_size(group)
+    if world == 1:
+        return record
+    gathered = record.new_empty(world * 32)
+    dist.all_gather_into_tensor(gathered, record, group=group)
+    return engine.reduce_records(gathered)
+
+
+def anneal_chains(engine: CloverEngine, starts, profile: ProfileTable, scenarios, ap: AnnealParams,
+                  seed: int, chain_base: int = 0, cluster: int = 8, log: bool = False, group=None,
+                  exchange: bool = True) -> ChainsResult:
+    """Batched Clover re-plan: every start graph is an independent chain.
+
+    Host buffers in, host results out: the starts are copied H2D from pinned memory,
+    all chains run to termination in one launch, the per-GPU winner is exchanged
+    across ranks (if a process group is up) and the results are copied D2H.
+    """
+    torch = engine.torch
+    if isinstance(starts, (list, tuple)) and starts and isinstance(starts[0], ConfigGraph):
+        starts = np.array([g.weights for g in starts], dtype=np.uint16)
+    host = torch.from_numpy(np.ascontiguousarray(np.asarray(starts, dtype=np.uint16)).view(np.int16))
+    host = host.pin_memory() if not host.is_pinned() else host
+    dev = host.to(device="cuda:%d" % engine.device, non_blocking=True).view(torch.uint16)
+    batch = engine.anneal(dev, profile, scenarios, ap, seed, chain_base=chain_base, cluster=cluster, log=log)
+    rec = engine.select_chains(batch)
+    if exchange:
+        rec = exchange_record(engine, rec, group)
+    out = batch.host()
+    record = np.frombuffer(rec.cpu().numpy().tobytes(), dtype=RECORD_DTYPE)[0]
+    res = out["results"]
+    local = int(record["index"]) - chain_base
+    if not 0 <= local < len(res):        # the winner lives on another rank: report ours
+        local = int(np.lexsort((np.arange(len(res)), res["h"], res["sla_met"] == 0))[0])
+    g = ConfigGraph(out["best_w"][local].astype(np.int64), profile.variant_count, profile.name)
+    return ChainsResult(_result_from_chain(res[local], g), chain_base + local, res, out["best_w"],
+                        out["final_w"], int(res["evals"].sum()), record, out.get("log"))
+
+
+def anneal(start: ConfigGraph, n: int, profile: ProfileTable, workload: Workload, ci: float,
+           obj: ObjectiveParams, ap: Optional[AnnealParams] = None, rng=None,
+           engine: Optional[CloverEngine] = None):
+    """Clover SA: returns (best EvalResult, log rows, simulated optimisation time).
+
+    Default AnnealParams follow the SPEC literally: one uniformly sampled neighbour
+    per iteration, 45 simulated seconds per evaluation against a 300 s budget.
+    """
+    eng = engine or default_engine(profile.topology)
+    ap = ap or AnnealParams(proposal="uniform", evaluate="proposal")
+    sc = scenario_for(n, workload, ci, obj)
+    res = anneal_chains(eng, [start], profile, sc, ap, _seed_of(rng), log=True, exchange=False)
+    row = res.results[0]
+    if row["status"] < 0:
+        raise InfeasibleGraphError("start graph is not realizable on %d GPUs" % n)
+    steps = int(row["steps"])
+    log = [dict(zip(res.log.dtype.names, r.tolist())) for r in res.log[0][:steps]] if res.log is not None else []
+    n_evals = int(row["evals"]) if ap.evaluate == "proposal" else 1 + steps
+    return res.best, log, n_evals * ap.eval_cost_s
+
+
+def sample_neighbor(g: ConfigGraph, n: int, profile: ProfileTable, rng=None,
+                    engine: Optional[CloverEngine] = None) -> ConfigGraph:
+    """A uniformly random legal GED<=4 neighbour: one chain step with an
+    always-accept temperature, proposal = min-hash neighbour."""
+    eng = engine or default_engine(profile.topology)
+    V = profile.variant_count
+    probe = Scenario(n, 1.0, 0.0, ObjectiveParams(1.0, 1.0, 1.0, 0.5))
+    ap = AnnealParams(t_init=1e300, t_floor=1e300, cooling_step=1.0, max_steps=1, stall_limit=1 << 30,
+                      proposal="uniform", evaluate="proposal", time_budget_s=math.inf)
+    res = anneal_chains(eng, [g], profile, probe, ap, _seed_of(rng), exchange=False)
+    row = res.results[0]
+    if row["status"] < 0:
+        raise InfeasibleGraphError("graph is not realizable on %d GPUs" % n)
+    if row["status"] == 2:
+        raise NoNeighborError("no legal neighbour")
+    return ConfigGraph(res.final_w[0].astype(np.int64), V, profile.name)
+
+
+def oracle_search(n: int, profile: ProfileTable, workload: Workload, ci: float, obj: ObjectiveParams,
+                  engine: Optional[CloverEngine] = None) -> EvalResult:
+    """Exhaustive standardized search on the device."""
+    eng = engine or default_engine(profile.topology)
+    sc = scenario_for(n, workload, ci, obj)
+    best = eng.oracle_search(profile, sc)
+    cid, assign = eng.oracle_decode(profile, best["index"])
+    fc = FleetConfig([cid] * n, list(assign) * n, profile.topology)
+    return EvalResult(build_graph(fc, profile), best["accuracy"], best["energy_wh"], best["p95_ms"],
+                      best["f"], best["h"], bool(best["sla_met"]))
+
+
+def blover_search(n: int, profile: ProfileTable, workload: Workload, ci: float, obj: ObjectiveParams,
+                  ap: Optional[AnnealParams] = None, rng=None, engine: Optional[CloverEngine] = None):
+    """Random search in x-space with anneal's termination rules."""
+    eng = engine or default_engine(profile.topology)
+    ap = ap or AnnealParams(proposal="uniform", evaluate="proposal")
+    sc = scenario_for(n, workload, ci, obj)
+    seed = _seed_of(rng)
+    budget = max(1, math.ceil(ap.time_budget_s / ap.eval_cost_s)) if ap.eval_cost_s > 0 else ap.max_steps + 1
+    budget = min(budget, ap.max_steps + 1)
+    pods = [(profile, sc, n, 1.0)]
+    _best, outs = eng.sweep(pods, 0, budget, seed, outputs=True)
+    h = outs["h"].cpu().numpy()
+    f = outs["f"].cpu().numpy()
+    sla = outs["sla"].cpu().numpy().astype(bool)
+    log, bi, stall = [], None, 0
+    for i in range(budget):
+        better = bi is None or (sla[i] and not sla[bi]) or (sla[i] == sla[bi] and h[i] < h[bi])
+        if better:
+            bi, stall = i, 0
+        else:
+            stall += 1
+        log.append(dict(iter=i, f=float(f[i]), h=float(h[i]), sla_met=bool(sla[i]), new_best=bool(better)))
+        if stall >= ap.stall_limit:
+            break
+    fc = eng.sweep_decode(pods, seed, bi)[0]
+    best, _ = eng.score_fleets([fc], profile, sc)
+    return EvalResult(build_graph(fc, profile), best["accuracy"], best["energy_wh"], best["p95_ms"],
+                      best["f"], best["h"], bool(best["sla_met"])), log
+
+
+def random_fleets(engine: CloverEngine, profile: ProfileTable, n: int, seed: int, count: int,
+                  first: int = 0) -> list[FleetConfig]:
+    """Counter-RNG x-space draws (the BLOVER sampler): config id uniform per GPU,
+    memory-feasible variant uniform per slice."""
+    probe = Scenario(n, 1.0, 0.0, ObjectiveParams(1.0, 1.0, 1.0, 0.5))
+    pods = [(profile, probe, n, 1.0)]
+    return [engine.sweep_decode(pods, seed, first + i)[0] for i in range(count)]
