@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="clover", choices=["clover", "reference"])
     ap.add_argument("--chains", type=int, default=CHAINS_PER_GPU)
-    ap.add_argument("--cluster", type=int, default=8)
+    ap.add_argument("--cluster", type=int, default=0, help="CTAs per chain (0 = auto: one wave)")
     ap.add_argument("--max-steps", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -77,20 +77,34 @@ def make_starts(engine, profile, seed, first, count):
 
 
 class ClockSampler:
+    """nvidia-smi sampler (the recipe's clocks line); samples are kept with wall timestamps
+    so only those inside the load window are summarised."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
     def __init__(self, index, path):
         self.path = path
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.fh = open(path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + q,
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
-    def stop(self):
+    def wait_first(self, timeout=5.0):
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < timeout:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    return
+            except OSError:
+                pass
+            time.sleep(0.02)
+
+    def stop(self, t_lo=None, t_hi=None):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -99,21 +113,26 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.fh.close()
-        sm, mx, reasons = [], None, set()
+        import datetime
+        sm, mx, reasons, power = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
+            if len(parts) < 10:
                 continue
             try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                clk, mxv, pw = float(parts[2]), float(parts[3]), float(parts[4])
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[5:9]):
+            if t_lo is not None and not (t_lo <= ts <= t_hi):
+                continue
+            sm.append(clk); mx = mxv; power.append(pw)
+            for nm, val in zip(names, parts[6:10]):
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "power_w_median": statistics.median(power) if power else None,
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
@@ -278,8 +297,15 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local, os.path.join(ROOT, "gpurun_out", "clocks_rank%d.csv" % rank)) \
-        if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else ClockSampler(local, "/tmp/clv_clocks_%d.csv" % rank)
+    clk_path = os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp",
+                            "clocks_rank%d.csv" % rank)
+    clocks = ClockSampler(local, clk_path)
+    clocks.wait_first()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_lo = time.time()
     t_wall0 = time.perf_counter()
     for s in range(args.warmup, total_steps):
         flush.zero_()
@@ -289,7 +315,14 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall0
-    clk = clocks.stop()
+    # keep the same load on the GPU (untimed repeats of the timed steps) so the
+    # clock sampler sees at least ~1 s of the workload
+    spare = [None] * total_steps
+    while time.time() - t_lo < 1.0:
+        for s in range(args.warmup, total_steps):
+            eng.anneal(starts_dev[s], prof, sc, ap, SEED + s, chain_base=base, cluster=args.cluster)
+        torch.cuda.synchronize()
+    clk = clocks.stop(t_lo, time.time())
     step_ms = [ev[s][0].elapsed_time(ev[s][2]) for s in range(args.warmup, total_steps)]
     anneal_ms = [ev[s][0].elapsed_time(ev[s][1]) for s in range(args.warmup, total_steps)]
     evals = sum(int(batches[s].host()["results"]["evals"].sum()) for s in range(args.warmup, total_steps))

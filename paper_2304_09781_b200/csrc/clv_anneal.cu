@@ -1,19 +1,23 @@
 // clv_anneal.cu -- K3 (GED<=4 neighbour generation + incremental scoring) fused
-// with K4 (warp-shuffle argmax) and K5 (anneal step), one thread-block CLUSTER
-// per annealing chain, every step of the chain inside one persistent launch.
+// with K4 (warp-shuffle argmax) and K5 (anneal step): one thread-block CLUSTER
+// per annealing chain, every step of every chain inside one persistent launch.
 //
 // Reference semantics: sample_neighbor, anneal
 // (SPEC:461-469, 478-483), Eqs. 6-7.  Step definition: DESIGN.md
 // "Chain step"; CPU restatement: oracle/anneal.py + oracle/neighbours.py.
 //
-// Layout per CTA (shared memory): the family's per-edge rows {thr, acc, en,
-// idle} (int64 fixed point), latency ranks, memory-feasible adjacency lists,
-// the chain centre (weights, exact int64 aggregates, presence mask by latency
-// rank), the compacted present-edge and removal-pair lists and the slice-delta
-// feasibility bytes of this step.  Each CTA of the cluster holds a full copy of
-// the centre and scores a strided share of the move space; CTA records meet in
-// the leader CTA's shared memory over DSMEM; the leader decides (Eq. 7), and
-// every CTA applies the accepted move locally.
+// Per CTA (shared memory): per-edge addition rows {thr, acc, en, idle} held as
+// fp64 *integers* (exact: every partial sum < 2^53, so any summation order
+// gives the same bits as the oracle's int64 W @ rows), latency-rank bits,
+// adjacency masks and memory-feasible neighbour lists; the centre; and per
+// step the removal table -- one entry per present edge (singles) and per
+// available removal pair (doubles) carrying the removal deltas, the presence
+// mask after removal and the canonical index base.  A neighbour is then
+//   S' = S + removal.d + row[a1] (+ row[a2]),  mask' = removal.m | bit(a1) | bit(a2)
+// followed by the fp64 epilogue.  Every CTA of the cluster builds identical
+// tables (ordered compaction) and scores a strided share of the move space;
+// CTA records meet in the leader CTA over DSMEM; the leader applies Eq. 7 and
+// broadcasts the accepted move, which every CTA applies to its own centre.
 #include <cooperative_groups.h>
 #include "clv_internal.h"
 
@@ -24,115 +28,150 @@ namespace clv {
 constexpr int ANT = 256;                  // threads per CTA
 constexpr int NWARP = ANT / 32;
 constexpr int MAXP = CLV_MAX_EDGES * (CLV_MAX_EDGES + 1) / 2;   // 820 removal pairs
-constexpr uint32_t NOMOVE = 0xFFFFFFFFu;
+constexpr int MAXCL = 16;
+constexpr long long NOIDX = -1;
 
-struct __align__(16) EdgeRow {
-    long long thr, acc, en, idle;
+enum { MODE_BEST_ALL = 0, MODE_UNIFORM_ALL = 1, MODE_UNIFORM_PROPOSAL = 2 };
+
+struct __align__(16) ARow {
+    double thr, acc, en, idle;
 };
 
-struct Decision {
-    uint32_t mv;
-    int done;
+struct __align__(8) RemEnt {            // one removal multiset R (single edge or pair)
+    double d0, d1, d2, d3;                 // -(rows of R), exact integers
+    unsigned long long mR;                 // presence mask (by latency rank) after removal
+    int base;                              // canonical index of (R, A = {})
+    unsigned short code;                   // slice code of R: sr1*125 + sr2*25 (doubles), sr*5 (singles)
+    unsigned char r1, r2, c1, c2;          // removed edges and their neighbour counts
 };
+
+struct KRec {                              // (key, idx) record; payload hv in uniform mode
+    unsigned long long key;
+    long long idx;
+    double hv;
+};
+
+__device__ __forceinline__ bool krec_less(unsigned long long ka, long long ia, const KRec &b) {
+    return ka < b.key || (ka == b.key && ia < b.idx);
+}
+__device__ __forceinline__ KRec krec_none() {
+    KRec r; r.key = ~0ULL; r.idx = 0x7FFFFFFFFFFFFFFFLL; r.hv = 0.0; return r;
+}
+__device__ __forceinline__ KRec krec_min_warp(KRec r) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        KRec o;
+        o.key = __shfl_xor_sync(0xFFFFFFFFu, r.key, m);
+        o.idx = __shfl_xor_sync(0xFFFFFFFFu, r.idx, m);
+        o.hv = __shfl_xor_sync(0xFFFFFFFFu, r.hv, m);
+        if (krec_less(o.key, o.idx, r)) r = o;
+    }
+    return r;
+}
 
 struct __align__(16) AnnealSmem {
-    EdgeRow row[CLV_MAX_EDGES];
+    ARow row[CLV_MAX_EDGES];
     double lat_by_rank[CLV_MAX_EDGES];
+    unsigned long long rbit[CLV_MAX_EDGES];
+    unsigned long long adjm[CLV_MAX_EDGES];
+    EvalConst ec;
     unsigned long long mem_ok;
-    unsigned char rank[CLV_MAX_EDGES];
+    short Pt[CLV_MAX_EDGES + 1];           // P(x, y) = Pt[x] + y
+    unsigned char sl[CLV_MAX_EDGES];
     unsigned char nb_cnt[CLV_MAX_EDGES];
     unsigned char nb[CLV_MAX_EDGES][CLV_NBMAX];
     unsigned short ij_tab[CLV_NBMAX * CLV_NBMAX];
     unsigned short pair_tab[MAXP];
     // centre
     int w[CLV_MAX_EDGES];
-    long long S[4];
+    double S[4];
     int svec[CLV_K];
     unsigned long long pmask;
-    unsigned char pe[CLV_MAX_EDGES];
-    unsigned short rp[MAXP];
+    // per-step tables
+    RemEnt se[CLV_MAX_EDGES];
+    RemEnt rp[MAXP];
     int nPE, nRP;
+    int warp_off[NWARP + 1];
     unsigned char feasS[25];
     unsigned char feasD[625];
     // reduction
-    Rec wr0[NWARP], wr1[NWARP];
+    KRec wS[NWARP], wV[NWARP], wP[NWARP];
     unsigned long long wc[NWARP];
-    // leader-only: one slot per cluster rank
-    Rec slot0[16], slot1[16];
-    unsigned long long slotc[16];
-    Decision dec;
-    // leader bookkeeping
+    // leader-only slots, one per cluster rank
+    KRec slS[MAXCL], slV[MAXCL], slP[MAXCL];
+    unsigned long long slc[MAXCL];
+    long long dec_move;                    // accepted move index, -1 = none
+    int dec_done;
     int bw[CLV_MAX_EDGES];
 };
 
-__device__ inline bool adjacent(int x, int y) {
-    return x != y && ((x / 5) == (y / 5) || (x % 5) == (y % 5));
+__device__ __forceinline__ double lmax_of(const AnnealSmem &s, unsigned long long m) {
+    return s.lat_by_rank[63 - __clzll((long long)m)];
 }
 
-// Score the centre's aggregates shifted by a move (a1,a2 added; r1,r2 removed;
-// 0xFF = absent).  Returns the presence mask of the neighbour too.
-__device__ inline Score score_move(const AnnealSmem &s, int r1, int r2, int a1, int a2,
-                                   const EvalConst &ec) {
-    long long t = s.S[0], ac = s.S[1], en = s.S[2], id = s.S[3];
+// canonical index -> move (r1, r2, a1, a2; 0xFF = absent)
+__device__ inline void decode_move(const AnnealSmem &s, int E, long long idx, int &r1, int &r2, int &a1, int &a2) {
+    if (idx < (long long)E * E) {
+        r1 = (int)(idx / E); a1 = (int)(idx % E); r2 = 0xFF; a2 = 0xFF;
+        return;
+    }
+    const int NP = E * (E + 1) / 2;
+    long long u = idx - (long long)E * E;
+    int p = (int)(u / NP), q = (int)(u % NP);
+    int x = 0;
+    while (x + 1 < E && s.Pt[x + 1] + x + 1 <= p) ++x;
+    r1 = x; r2 = p - s.Pt[x];
+    x = 0;
+    while (x + 1 < E && s.Pt[x + 1] + x + 1 <= q) ++x;
+    a1 = x; a2 = q - s.Pt[x];
+}
+
+__device__ inline Score score_move(const AnnealSmem &s, int r1, int r2, int a1, int a2) {
+    double t = s.S[0], ac = s.S[1], en = s.S[2], id = s.S[3];
     unsigned long long m = s.pmask;
-    if (r1 != 0xFF) {
-        t -= s.row[r1].thr; ac -= s.row[r1].acc; en -= s.row[r1].en; id -= s.row[r1].idle;
+    int e[2] = {r1, r2};
+    for (int k = 0; k < 2; ++k) {
+        if (e[k] == 0xFF) continue;
+        t -= s.row[e[k]].thr; ac -= s.row[e[k]].acc; en -= s.row[e[k]].en; id -= s.row[e[k]].idle;
     }
-    if (r2 != 0xFF) {
-        t -= s.row[r2].thr; ac -= s.row[r2].acc; en -= s.row[r2].en; id -= s.row[r2].idle;
+    if (r1 != 0xFF && s.w[r1] - 1 - (r2 == r1 ? 1 : 0) == 0) m &= ~s.rbit[r1];
+    if (r2 != 0xFF && r2 != r1 && s.w[r2] - 1 == 0) m &= ~s.rbit[r2];
+    int f[2] = {a1, a2};
+    for (int k = 0; k < 2; ++k) {
+        if (f[k] == 0xFF) continue;
+        t += s.row[f[k]].thr; ac += s.row[f[k]].acc; en += s.row[f[k]].en; id += s.row[f[k]].idle;
+        m |= s.rbit[f[k]];
     }
-    if (r1 != 0xFF) {
-        int left = s.w[r1] - 1 - (r2 == r1 ? 1 : 0);
-        if (left == 0) m &= ~(1ULL << s.rank[r1]);
-    }
-    if (r2 != 0xFF && r2 != r1) {
-        if (s.w[r2] - 1 == 0) m &= ~(1ULL << s.rank[r2]);
-    }
-    if (a1 != 0xFF) {
-        t += s.row[a1].thr; ac += s.row[a1].acc; en += s.row[a1].en; id += s.row[a1].idle;
-        m |= 1ULL << s.rank[a1];
-    }
-    if (a2 != 0xFF) {
-        t += s.row[a2].thr; ac += s.row[a2].acc; en += s.row[a2].en; id += s.row[a2].idle;
-        m |= 1ULL << s.rank[a2];
-    }
-    double lmax = s.lat_by_rank[63 - __clzll((long long)m)];
-    return epilogue(t, ac, en, id, lmax, ec);
-}
-
-__device__ inline void unpack_mv(uint32_t mv, int &r1, int &r2, int &a1, int &a2) {
-    r1 = mv & 0xFF; r2 = (mv >> 8) & 0xFF; a1 = (mv >> 16) & 0xFF; a2 = (mv >> 24) & 0xFF;
+    return epilogue_d(t, ac, en, id, lmax_of(s, m), s.ec);
 }
 
 // Apply a move to the CTA-local centre (thread 0) -- O(1).
-__device__ inline void apply_move(AnnealSmem &s, uint32_t mv) {
+__device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
     int r[2], a[2];
-    unpack_mv(mv, r[0], r[1], a[0], a[1]);
+    decode_move(s, E, idx, r[0], r[1], a[0], a[1]);
     for (int k = 0; k < 2; ++k) {
         if (r[k] == 0xFF) continue;
         int e = r[k];
         s.w[e] -= 1;
         s.S[0] -= s.row[e].thr; s.S[1] -= s.row[e].acc; s.S[2] -= s.row[e].en; s.S[3] -= s.row[e].idle;
-        s.svec[e % 5] -= 1;
-        if (s.w[e] == 0) s.pmask &= ~(1ULL << s.rank[e]);
+        s.svec[s.sl[e]] -= 1;
+        if (s.w[e] == 0) s.pmask &= ~s.rbit[e];
     }
     for (int k = 0; k < 2; ++k) {
         if (a[k] == 0xFF) continue;
         int e = a[k];
         s.w[e] += 1;
         s.S[0] += s.row[e].thr; s.S[1] += s.row[e].acc; s.S[2] += s.row[e].en; s.S[3] += s.row[e].idle;
-        s.svec[e % 5] += 1;
-        s.pmask |= 1ULL << s.rank[e];
+        s.svec[s.sl[e]] += 1;
+        s.pmask |= s.rbit[e];
     }
 }
 
-// Rebuild the present-edge list, the removal-pair list and the feasibility
-// bytes of all 25 single / 625 double slice deltas (all threads).
+// Per-step tables: ordered (deterministic) compaction of the removal pairs and
+// present edges -- every CTA of the cluster must build identical tables because
+// the cluster partitions the move space by table position -- plus the
+// feasibility bytes of all 25 single / 625 double slice deltas.
 __device__ inline void prepare_step(AnnealSmem &s, int E, int n, const FeasView &F) {
-    // Ordered (deterministic) compaction: every CTA of the cluster must build
-    // identical lists, because the cluster partitions the move space by list
-    // position.
-    __shared__ int warp_off[NWARP + 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int NP = E * (E + 1) / 2;
     int base = 0;
@@ -146,16 +185,33 @@ __device__ inline void prepare_step(AnnealSmem &s, int E, int n, const FeasView 
             ok = (x == y) ? (wx >= 2) : (wx > 0 && wy > 0);
         }
         const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
-        if (lane == 0) warp_off[wid] = __popc(bal);
+        if (lane == 0) s.warp_off[wid] = __popc(bal);
         __syncthreads();
         if (threadIdx.x == 0) {
             int acc = 0;
-            for (int q = 0; q < NWARP; ++q) { int c = warp_off[q]; warp_off[q] = acc; acc += c; }
-            warp_off[NWARP] = acc;
+            for (int q = 0; q < NWARP; ++q) { int c = s.warp_off[q]; s.warp_off[q] = acc; acc += c; }
+            s.warp_off[NWARP] = acc;
         }
         __syncthreads();
-        if (ok) s.rp[base + warp_off[wid] + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)(x | (y << 8));
-        base += warp_off[NWARP];
+        if (ok) {
+            RemEnt &r = s.rp[base + s.warp_off[wid] + __popc(bal & ((1u << lane) - 1u))];
+            r.d0 = -(s.row[x].thr + s.row[y].thr);
+            r.d1 = -(s.row[x].acc + s.row[y].acc);
+            r.d2 = -(s.row[x].en + s.row[y].en);
+            r.d3 = -(s.row[x].idle + s.row[y].idle);
+            unsigned long long m = s.pmask;
+            if (x == y) { if (s.w[x] == 2) m &= ~s.rbit[x]; }
+            else {
+                if (s.w[x] == 1) m &= ~s.rbit[x];
+                if (s.w[y] == 1) m &= ~s.rbit[y];
+            }
+            r.mR = m;
+            r.base = E * E + (s.Pt[x] + y) * NP;
+            r.code = (unsigned short)(s.sl[x] * 125 + s.sl[y] * 25);
+            r.r1 = (unsigned char)x; r.r2 = (unsigned char)y;
+            r.c1 = s.nb_cnt[x]; r.c2 = s.nb_cnt[y];
+        }
+        base += s.warp_off[NWARP];
         __syncthreads();
     }
     if (wid == 0) {
@@ -164,7 +220,14 @@ __device__ inline void prepare_step(AnnealSmem &s, int E, int n, const FeasView 
             const int e = e0 + lane;
             const bool ok = e < E && s.w[e] > 0;
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
-            if (ok) s.pe[cnt + __popc(bal & ((1u << lane) - 1u))] = (unsigned char)e;
+            if (ok) {
+                RemEnt &r = s.se[cnt + __popc(bal & ((1u << lane) - 1u))];
+                r.d0 = -s.row[e].thr; r.d1 = -s.row[e].acc; r.d2 = -s.row[e].en; r.d3 = -s.row[e].idle;
+                r.mR = (s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask;
+                r.base = e * E;
+                r.code = (unsigned short)(s.sl[e] * 5);
+                r.r1 = (unsigned char)e; r.r2 = 0xFF; r.c1 = 0; r.c2 = 0;
+            }
             cnt += __popc(bal);
         }
         if (lane == 0) { s.nPE = cnt; s.nRP = base; }
@@ -175,38 +238,39 @@ __device__ inline void prepare_step(AnnealSmem &s, int E, int n, const FeasView 
         for (int k = 0; k < CLV_K; ++k) v[k] = s.svec[k];
         if (t < 25) {
             v[t / 5] -= 1; v[t % 5] += 1;
-            bool ok = v[t / 5] >= 0 && feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
-            s.feasS[t] = ok;
+            s.feasS[t] = v[t / 5] >= 0 && feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
         } else {
-            int u = t - 25;
+            const int u = t - 25;
             v[u / 125] -= 1; v[(u / 25) % 5] -= 1; v[(u / 5) % 5] += 1; v[u % 5] += 1;
-            bool ok = v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[3] >= 0 && v[4] >= 0 &&
-                      feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
-            s.feasD[u] = ok;
+            s.feasD[u] = v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[3] >= 0 && v[4] >= 0 &&
+                         feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
         }
     }
     __syncthreads();
 }
 
-__device__ inline void init_centre(AnnealSmem &s, const uint16_t *w0, int E) {
-    if (threadIdx.x == 0) {
-        long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
-        unsigned long long m = 0;
-        for (int k = 0; k < CLV_K; ++k) s.svec[k] = 0;
-        for (int e = 0; e < E; ++e) {
-            int x = w0[e];
-            s.w[e] = x;
-            S0 += (long long)x * s.row[e].thr; S1 += (long long)x * s.row[e].acc;
-            S2 += (long long)x * s.row[e].en; S3 += (long long)x * s.row[e].idle;
-            s.svec[e % 5] += x;
-            if (x > 0) m |= 1ULL << s.rank[e];
+// Fold one valid neighbour into the thread's records.
+template <int MODE>
+__device__ __forceinline__ void fold(const AnnealSmem &s, double t, double ac, double en, double id,
+                                     unsigned long long m, long long idx, KRec &rS, KRec &rV, KRec &rP,
+                                     uint64_t seed, uint64_t gchain, uint64_t k) {
+    if (MODE != MODE_UNIFORM_PROPOSAL) {
+        const Score sc = epilogue_d(t, ac, en, id, lmax_of(s, m), s.ec);
+        const unsigned long long key = okey(sc.h);
+        if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; } }
+        else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; } }
+        if (MODE == MODE_UNIFORM_ALL) {
+            const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
+            if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; rP.hv = sc.h; }
         }
-        s.S[0] = S0; s.S[1] = S1; s.S[2] = S2; s.S[3] = S3;
-        s.pmask = m;
+    } else {
+        const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
+        if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; }
     }
 }
 
-__global__ void __launch_bounds__(ANT) anneal_kernel(const __grid_constant__ AnnealArgs args) {
+template <int MODE>
+__global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ AnnealArgs args) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     AnnealSmem &s = *reinterpret_cast<AnnealSmem *>(smem_raw);
     cg::cluster_group cluster = cg::this_cluster();
@@ -214,196 +278,218 @@ __global__ void __launch_bounds__(ANT) anneal_kernel(const __grid_constant__ Ann
     const int crank = (int)cluster.block_rank();
     const int chain = blockIdx.x / CL;
     if (chain >= args.n_chains) return;      // whole cluster exits together
-    const long long gchain = args.chain_base + chain;
+    const uint64_t gchain = (uint64_t)(args.chain_base + chain);
     const FamilyTables &T = *args.fam;
     const int E = T.E;
     const int n = args.n;
-    const EvalConst ec = args.ec[args.n_ec == 1 ? 0 : chain];
     const int tid = threadIdx.x;
 
     // ---- stage tables
     for (int e = tid; e < E; e += ANT) {
-        s.row[e].thr = T.thr_q[e];
-        s.row[e].acc = T.acc_q[e];
-        s.row[e].en = T.en_q[e];
-        s.row[e].idle = T.idle_q[e % 5];
+        s.row[e].thr = (double)T.thr_q[e];
+        s.row[e].acc = (double)T.acc_q[e];
+        s.row[e].en = (double)T.en_q[e];
+        s.row[e].idle = (double)T.idle_q[e % 5];
         s.lat_by_rank[e] = T.lat_by_rank[e];
-        s.rank[e] = T.rank[e];
+        s.rbit[e] = 1ULL << T.rank[e];
+        s.sl[e] = (unsigned char)(e % 5);
         s.nb_cnt[e] = T.nb_cnt[e];
+        unsigned long long am = 0;
+        for (int x = 0; x < E; ++x)
+            if (x != e && (x / 5 == e / 5 || x % 5 == e % 5)) am |= 1ULL << x;
+        s.adjm[e] = am;
         for (int k = 0; k < CLV_NBMAX; ++k) s.nb[e][k] = T.nb[e][k];
     }
+    for (int x = tid; x <= E; x += ANT) s.Pt[x] = (short)(x * E - (x * (x - 1)) / 2 - x);
     const int nbm = T.nbmax;
     const int NB2 = nbm * nbm;
     for (int t = tid; t < NB2; t += ANT) s.ij_tab[t] = (unsigned short)(((t / nbm) << 8) | (t % nbm));
     for (int x = tid; x < E; x += ANT)
-        for (int y = x; y < E; ++y) s.pair_tab[pair_index(x, y, E)] = (unsigned short)(x | (y << 8));
-    if (tid == 0) s.mem_ok = T.mem_ok;
+        for (int y = x; y < E; ++y) s.pair_tab[x * E - (x * (x - 1)) / 2 + (y - x)] = (unsigned short)(x | (y << 8));
+    if (tid == 0) {
+        s.mem_ok = T.mem_ok;
+        s.ec = args.ec[args.n_ec == 1 ? 0 : chain];
+    }
     __syncthreads();
-    init_centre(s, args.start_w + (size_t)chain * E, E);
+    if (tid == 0) {
+        const uint16_t *w0 = args.start_w + (size_t)chain * E;
+        double S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+        unsigned long long m = 0;
+        for (int k = 0; k < CLV_K; ++k) s.svec[k] = 0;
+        for (int e = 0; e < E; ++e) {
+            const int x = w0[e];
+            s.w[e] = x;
+            S0 += x * s.row[e].thr; S1 += x * s.row[e].acc; S2 += x * s.row[e].en; S3 += x * s.row[e].idle;
+            s.svec[e % 5] += x;
+            if (x > 0) m |= s.rbit[e];
+        }
+        s.S[0] = S0; s.S[1] = S1; s.S[2] = S2; s.S[3] = S3;
+        s.pmask = m;
+    }
     __syncthreads();
 
     // ---- leader state (thread 0 of rank 0)
     const bool leader = (crank == 0 && tid == 0);
-    double hc = 0.0, fc = 0.0, Lc = 0.0;
-    bool slac = false;
-    uint32_t bk1 = 0; uint64_t bk2 = 0;
+    double hc = 0.0;
+    unsigned int bk1 = 0;
+    unsigned long long bk2 = 0;
     int best_step = -1, stall = 0, steps = 0, status = 0;
     long long best_idx = -1, evals = 1;
-    int invalid = 0;
     if (leader) {
-        // start validity: memory-feasible edges only, fleet-feasible slice multiset
+        int invalid = 0;
         long long tot = 0;
         for (int e = 0; e < E; ++e) {
             tot += s.w[e];
             if (s.w[e] > 0 && !((s.mem_ok >> e) & 1ULL)) invalid = 1;
         }
-        if (tot < 1 || !feasible(args.F, n, s.svec[0], s.svec[1], s.svec[2], s.svec[3], s.svec[4]))
-            invalid = 1;
-        double lmax = s.lat_by_rank[63 - __clzll((long long)(s.pmask | 1ULL))];
-        Score sc = epilogue(s.S[0], s.S[1], s.S[2], s.S[3], lmax, ec);
-        hc = sc.h; fc = sc.f; Lc = sc.L; slac = sc.sla;
+        if (tot < 1 || !feasible(args.F, n, s.svec[0], s.svec[1], s.svec[2], s.svec[3], s.svec[4])) invalid = 1;
+        const Score sc = epilogue_d(s.S[0], s.S[1], s.S[2], s.S[3], lmax_of(s, s.pmask | 1ULL), s.ec);
+        hc = sc.h;
         bk1 = sc.sla ? 0u : 1u; bk2 = okey(sc.h);
         for (int e = 0; e < E; ++e) s.bw[e] = s.w[e];
-        s.dec.mv = NOMOVE;
-        s.dec.done = invalid || (args.max_steps <= 0);
+        s.dec_move = NOIDX;
+        s.dec_done = invalid || (args.max_steps <= 0);
         if (invalid) status = -1;
     }
     cluster.sync();
-    if (tid == 0 && crank != 0) s.dec = *cluster.map_shared_rank(&s.dec, 0);
+    if (tid == 0 && crank != 0) s.dec_done = *cluster.map_shared_rank(&s.dec_done, 0);
     __syncthreads();
-    bool done = s.dec.done;
-    const bool eval_all = (args.evaluate == 0);
-    const bool uniform = (args.proposal == 1);
+    bool done = s.dec_done;
     const int G = CL * ANT;
     const int gt = crank * ANT + tid;
     const unsigned long long mem_ok = s.mem_ok;
 
     for (int k = 0; !done; ++k) {
         prepare_step(s, E, n, args.F);
-        // -------- score this CTA's share of the neighbourhood
-        Rec cand = rec_none(), prop = rec_none();
+        KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
         unsigned long long cnt = 0;
-        const int nS = s.nPE * E;
-        for (int t = gt; t < nS; t += G) {
-            int i = t / E, a = t - i * E;
-            int r = s.pe[i];
-            if (a == r || !((mem_ok >> a) & 1ULL)) continue;
-            if (!s.feasS[(r % 5) * 5 + (a % 5)]) continue;
-            ++cnt;
-            long long idx = (long long)r * E + a;
-            uint32_t mv = (uint32_t)r | 0xFF00u | ((uint32_t)a << 16) | 0xFF000000u;
-            Rec rc;
-            rc.idx = idx; rc.mv = mv;
-            if (eval_all) {
-                Score sc = score_move(s, r, 0xFF, a, 0xFF, ec);
-                rc.hv = sc.h;
-                rc.k1 = sc.sla ? 0u : 1u; rc.k2 = okey(sc.h);
-                if (rec_less(rc, cand)) cand = rc;
-                rc.k1 = 0u;
-                if (uniform) rc.k2 = derive_seed4(args.seed, (uint64_t)gchain, (uint64_t)k, (uint64_t)idx + 1);
-                if (rec_less(rc, prop)) prop = rc;
-            } else {
-                rc.hv = 0.0; rc.k1 = 0u;
-                rc.k2 = derive_seed4(args.seed, (uint64_t)gchain, (uint64_t)k, (uint64_t)idx + 1);
-                if (rec_less(rc, prop)) prop = rc;
-            }
-        }
-        const int nD = s.nRP * NB2;
-        const int NP = E * (E + 1) / 2;
-        for (int u = gt; u < nD; u += G) {
-            int j = u / NB2, ij = u - j * NB2;
-            int r1 = s.rp[j] & 0xFF, r2 = s.rp[j] >> 8;
-            int ii = s.ij_tab[ij] >> 8, jj = s.ij_tab[ij] & 0xFF;
-            if (ii >= s.nb_cnt[r1] || jj >= s.nb_cnt[r2]) continue;
-            int a1 = s.nb[r1][ii], a2 = s.nb[r2][jj];
-            if (a1 == r2 || a2 == r1) continue;
-            if (a1 > a2 && adjacent(r1, a2) && adjacent(r2, a1)) continue;
-            if (!s.feasD[(((r1 % 5) * 5 + (r2 % 5)) * 5 + (a1 % 5)) * 5 + (a2 % 5)]) continue;
-            ++cnt;
-            int lo = a1 < a2 ? a1 : a2, hi = a1 < a2 ? a2 : a1;
-            long long idx = (long long)E * E + (long long)pair_index(r1, r2, E) * NP + pair_index(lo, hi, E);
-            uint32_t mv = (uint32_t)r1 | ((uint32_t)r2 << 8) | ((uint32_t)a1 << 16) | ((uint32_t)a2 << 24);
-            Rec rc;
-            rc.idx = idx; rc.mv = mv;
-            if (eval_all) {
-                Score sc = score_move(s, r1, r2, a1, a2, ec);
-                rc.hv = sc.h;
-                rc.k1 = sc.sla ? 0u : 1u; rc.k2 = okey(sc.h);
-                if (rec_less(rc, cand)) cand = rc;
-                rc.k1 = 0u;
-                if (uniform) rc.k2 = derive_seed4(args.seed, (uint64_t)gchain, (uint64_t)k, (uint64_t)idx + 1);
-                if (rec_less(rc, prop)) prop = rc;
-            } else {
-                rc.hv = 0.0; rc.k1 = 0u;
-                rc.k2 = derive_seed4(args.seed, (uint64_t)gchain, (uint64_t)k, (uint64_t)idx + 1);
-                if (rec_less(rc, prop)) prop = rc;
-            }
-        }
-        // -------- CTA reduction
+        // ---- singles: (present edge i, target edge a)
         {
-            int lane = tid & 31, wid = tid >> 5;
-            cand = warp_min(cand);
-            prop = warp_min(prop);
+            const int nS = s.nPE * E;
+            int i = gt / E, a = gt - (gt / E) * E;
+            const int dI = G / E, dA = G - (G / E) * E;
+            for (int t = gt; t < nS; t += G) {
+                const RemEnt &R = s.se[i];
+                const bool ok = (a != R.r1) && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]];
+                if (ok) {
+                    ++cnt;
+                    const ARow &A = s.row[a];
+                    fold<MODE>(s, s.S[0] + R.d0 + A.thr, s.S[1] + R.d1 + A.acc, s.S[2] + R.d2 + A.en,
+                               s.S[3] + R.d3 + A.idle, R.mR | s.rbit[a], (long long)(R.base + a),
+                               rS, rV, rP, args.seed, gchain, (uint64_t)k);
+                }
+                i += dI; a += dA;
+                if (a >= E) { a -= E; ++i; }
+            }
+        }
+        // ---- doubles: (removal pair j, neighbour slots ij)
+        {
+            const int nD = s.nRP * NB2;
+            int j = gt / NB2, ij = gt - (gt / NB2) * NB2;
+            const int dJ = G / NB2, dIJ = G - (G / NB2) * NB2;
+            for (int u = gt; u < nD; u += G) {
+                const RemEnt &R = s.rp[j];
+                const unsigned short tij = s.ij_tab[ij];
+                const int ii = tij >> 8, jj = tij & 0xFF;
+                bool ok = ii < R.c1 && jj < R.c2;
+                if (ok) {
+                    const int a1 = s.nb[R.r1][ii], a2 = s.nb[R.r2][jj];
+                    ok = a1 != R.r2 && a2 != R.r1 &&
+                         !(a1 > a2 && ((s.adjm[R.r1] >> a2) & 1ULL) && ((s.adjm[R.r2] >> a1) & 1ULL)) &&
+                         s.feasD[R.code + s.sl[a1] * 5 + s.sl[a2]];
+                    if (ok) {
+                        ++cnt;
+                        const ARow &A1 = s.row[a1], &A2 = s.row[a2];
+                        const int lo = a1 < a2 ? a1 : a2, hi = a1 < a2 ? a2 : a1;
+                        fold<MODE>(s, s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
+                                   s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
+                                   R.mR | s.rbit[a1] | s.rbit[a2], (long long)(R.base + s.Pt[lo] + hi),
+                                   rS, rV, rP, args.seed, gchain, (uint64_t)k);
+                    }
+                }
+                j += dJ; ij += dIJ;
+                if (ij >= NB2) { ij -= NB2; ++j; }
+            }
+        }
+        // ---- CTA reduction, then DSMEM publish into the leader's slots
+        {
+            const int lane = tid & 31, wid = tid >> 5;
+            if (MODE != MODE_UNIFORM_PROPOSAL) { rS = krec_min_warp(rS); rV = krec_min_warp(rV); }
+            if (MODE != MODE_BEST_ALL) rP = krec_min_warp(rP);
 #pragma unroll
             for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, m);
-            if (lane == 0) { s.wr0[wid] = cand; s.wr1[wid] = prop; s.wc[wid] = cnt; }
+            if (lane == 0) { s.wS[wid] = rS; s.wV[wid] = rV; s.wP[wid] = rP; s.wc[wid] = cnt; }
             __syncthreads();
             if (wid == 0) {
-                cand = lane < NWARP ? s.wr0[lane] : rec_none();
-                prop = lane < NWARP ? s.wr1[lane] : rec_none();
+                rS = lane < NWARP ? s.wS[lane] : krec_none();
+                rV = lane < NWARP ? s.wV[lane] : krec_none();
+                rP = lane < NWARP ? s.wP[lane] : krec_none();
                 cnt = lane < NWARP ? s.wc[lane] : 0ULL;
-                cand = warp_min(cand);
-                prop = warp_min(prop);
+                if (MODE != MODE_UNIFORM_PROPOSAL) { rS = krec_min_warp(rS); rV = krec_min_warp(rV); }
+                if (MODE != MODE_BEST_ALL) rP = krec_min_warp(rP);
 #pragma unroll
                 for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, m);
                 if (lane == 0) {
                     AnnealSmem *ls = cluster.map_shared_rank(&s, 0);
-                    ls->slot0[crank] = cand;
-                    ls->slot1[crank] = prop;
-                    ls->slotc[crank] = cnt;
+                    ls->slS[crank] = rS; ls->slV[crank] = rV; ls->slP[crank] = rP; ls->slc[crank] = cnt;
                 }
             }
         }
         cluster.sync();
-        // -------- leader: decide
+        // ---- leader: best tracking, Eq. 7, termination
         if (leader) {
-            Rec C = rec_none(), P = rec_none();
+            KRec S = krec_none(), V = krec_none(), P = krec_none();
             unsigned long long total = 0;
             for (int q = 0; q < CL; ++q) {
-                if (rec_less(s.slot0[q], C)) C = s.slot0[q];
-                if (rec_less(s.slot1[q], P)) P = s.slot1[q];
-                total += s.slotc[q];
+                if (krec_less(s.slS[q].key, s.slS[q].idx, S)) S = s.slS[q];
+                if (krec_less(s.slV[q].key, s.slV[q].idx, V)) V = s.slV[q];
+                if (krec_less(s.slP[q].key, s.slP[q].idx, P)) P = s.slP[q];
+                total += s.slc[q];
             }
-            uint32_t mv_out = NOMOVE;
+            long long mv = NOIDX;
             int fin = 0;
             if (total == 0) {
                 status = 2;
                 fin = 1;
             } else {
-                double hp, fp = 0.0, Lp = 0.0;
+                // candidate for best tracking: SLA-meeting first
+                unsigned int ck1;
+                unsigned long long ck2;
+                long long cidx;
+                double hp;
+                long long pidx;
+                double fp = 0.0, Lp = 0.0;
                 bool slap = false;
-                int r1, r2, a1, a2;
-                unpack_mv(P.mv, r1, r2, a1, a2);
-                if (eval_all) {
+                if (MODE == MODE_UNIFORM_PROPOSAL) {
+                    evals += 1;
+                    int r1, r2, a1, a2;
+                    decode_move(s, E, P.idx, r1, r2, a1, a2);
+                    const Score sp = score_move(s, r1, r2, a1, a2);
+                    hp = sp.h; fp = sp.f; Lp = sp.L; slap = sp.sla;
+                    pidx = P.idx;
+                    ck1 = sp.sla ? 0u : 1u; ck2 = okey(sp.h); cidx = P.idx;
+                } else {
                     evals += (long long)total;
-                    hp = P.hv;
+                    if (S.idx != 0x7FFFFFFFFFFFFFFFLL) { ck1 = 0u; ck2 = S.key; cidx = S.idx; }
+                    else { ck1 = 1u; ck2 = V.key; cidx = V.idx; }
+                    if (MODE == MODE_BEST_ALL) {
+                        const KRec &B = krec_less(S.key, S.idx, V) ? S : V;   // min h overall
+                        pidx = B.idx; hp = okey_inv(B.key);
+                    } else {
+                        pidx = P.idx; hp = P.hv;
+                    }
                     if (args.log) {
-                        Score sp = score_move(s, r1, r2, a1, a2, ec);
+                        int r1, r2, a1, a2;
+                        decode_move(s, E, pidx, r1, r2, a1, a2);
+                        const Score sp = score_move(s, r1, r2, a1, a2);
                         fp = sp.f; Lp = sp.L; slap = sp.sla;
                     }
-                } else {
-                    evals += 1;
-                    Score sp = score_move(s, r1, r2, a1, a2, ec);
-                    hp = sp.h; fp = sp.f; Lp = sp.L; slap = sp.sla;
-                    C = P;
-                    C.k1 = sp.sla ? 0u : 1u;
-                    C.k2 = okey(sp.h);
                 }
-                bool nb = (C.k1 < bk1) || (C.k1 == bk1 && C.k2 < bk2);
+                const bool nb = (ck1 < bk1) || (ck1 == bk1 && ck2 < bk2);
                 if (nb) {
-                    bk1 = C.k1; bk2 = C.k2; best_step = k; best_idx = C.idx; stall = 0;
+                    bk1 = ck1; bk2 = ck2; best_step = k; best_idx = cidx; stall = 0;
                     int c1, c2, c3, c4;
-                    unpack_mv(C.mv, c1, c2, c3, c4);
+                    decode_move(s, E, cidx, c1, c2, c3, c4);
                     for (int e = 0; e < E; ++e) s.bw[e] = s.w[e];
                     if (c1 != 0xFF) s.bw[c1] -= 1;
                     if (c2 != 0xFF) s.bw[c2] -= 1;
@@ -412,56 +498,55 @@ __global__ void __launch_bounds__(ANT) anneal_kernel(const __grid_constant__ Ann
                 } else {
                     stall += 1;
                 }
-                double T0 = args.t_init - (double)k * args.cooling;
-                double Tk = args.t_floor >= T0 ? args.t_floor : T0;
-                double u = uniform01(derive_seed4(args.seed, (uint64_t)gchain, (uint64_t)k, 0ULL));
-                bool acc = (hp <= hc) || (u < exp_clv(-(hp - hc) / Tk));
+                const double T0 = args.t_init - (double)k * args.cooling;
+                const double Tk = args.t_floor >= T0 ? args.t_floor : T0;
+                const double u = uniform01(derive_seed4(args.seed, gchain, (uint64_t)k, 0ULL));
+                const bool acc = (hp <= hc) || (u < exp_clv(-(hp - hc) / Tk));
                 if (args.log) {
                     clv_log_row row;
                     row.temp = Tk; row.f = fp; row.h = hp; row.p95_ms = Lp;
-                    row.iter = k; row.ged_from_center = (r2 == 0xFF) ? 2 : 4; row.sla_met = slap;
+                    row.iter = k; row.ged_from_center = (pidx < (long long)E * E) ? 2 : 4; row.sla_met = slap;
                     row.accepted = acc; row.new_best = nb; row.n_neighbours = (int)total;
                     args.log[(size_t)chain * args.max_steps + k] = row;
                 }
-                if (acc) {
-                    hc = hp; fc = fp; Lc = Lp; slac = slap;
-                    mv_out = P.mv;
-                }
+                if (acc) { hc = hp; mv = pidx; }
                 steps = k + 1;
                 if (stall >= args.stall_limit) { status = 1; fin = 1; }
             }
             if (!fin && k + 1 >= args.max_steps) { status = 0; fin = 1; }
-            s.dec.mv = mv_out;
-            s.dec.done = fin;
+            s.dec_move = mv;
+            s.dec_done = fin;
         }
         cluster.sync();
         if (tid == 0) {
-            Decision d = (crank == 0) ? s.dec : *cluster.map_shared_rank(&s.dec, 0);
-            if (d.mv != NOMOVE) apply_move(s, d.mv);
-            s.dec = d;
+            long long mv;
+            int dn;
+            if (crank == 0) { mv = s.dec_move; dn = s.dec_done; }
+            else {
+                mv = *cluster.map_shared_rank(&s.dec_move, 0);
+                dn = *cluster.map_shared_rank(&s.dec_done, 0);
+                s.dec_move = mv; s.dec_done = dn;
+            }
+            if (mv != NOIDX) apply_move(s, E, mv);
         }
         __syncthreads();
-        done = s.dec.done;
-        // leader's slots are rewritten only after the next compute phase, which
-        // every CTA reaches after this point -- the second cluster.sync orders it.
+        done = s.dec_done;
     }
 
     if (leader) {
-        (void)fc; (void)Lc; (void)slac;
         clv_chain_result r;
         uint16_t *bw_out = args.best_w + (size_t)chain * E;
         uint16_t *fw_out = args.final_w + (size_t)chain * E;
-        long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+        double S0 = 0, S1 = 0, S2 = 0, S3 = 0;
         unsigned long long m = 0;
         for (int e = 0; e < E; ++e) {
-            int x = s.bw[e];
+            const int x = s.bw[e];
             bw_out[e] = (uint16_t)x;
             fw_out[e] = (uint16_t)s.w[e];
-            S0 += (long long)x * s.row[e].thr; S1 += (long long)x * s.row[e].acc;
-            S2 += (long long)x * s.row[e].en; S3 += (long long)x * s.row[e].idle;
-            if (x > 0) m |= 1ULL << s.rank[e];
+            S0 += x * s.row[e].thr; S1 += x * s.row[e].acc; S2 += x * s.row[e].en; S3 += x * s.row[e].idle;
+            if (x > 0) m |= s.rbit[e];
         }
-        Score sb = epilogue(S0, S1, S2, S3, s.lat_by_rank[63 - __clzll((long long)(m | 1ULL))], ec);
+        const Score sb = epilogue_d(S0, S1, S2, S3, lmax_of(s, m | 1ULL), s.ec);
         r.f = sb.f; r.h = sb.h; r.p95_ms = sb.L; r.accuracy = sb.A; r.energy_wh = sb.E;
         r.sla_met = sb.sla;
         r.status = status; r.steps = steps; r.best_step = best_step;
@@ -470,28 +555,47 @@ __global__ void __launch_bounds__(ANT) anneal_kernel(const __grid_constant__ Ann
     }
 }
 
-cudaError_t launch_anneal(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
-    size_t smem = sizeof(AnnealSmem);
-    cudaError_t e = cudaFuncSetAttribute(anneal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+template <int MODE>
+static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
+    const size_t smem = sizeof(AnnealSmem);
+    cudaError_t e = cudaFuncSetAttribute(anneal_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (cluster_size > 8) {
-        e = cudaFuncSetAttribute(anneal_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
+    e = cudaFuncSetAttribute(anneal_kernel<MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(a.n_chains * cluster_size), 1, 1);
     cfg.blockDim = dim3(ANT, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)cluster_size;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, anneal_kernel, a);
+    if (cluster_size <= 0) {
+        // Largest cluster size that still keeps every chain resident (one wave).
+        cluster_size = 1;
+        for (int c = 16; c >= 2; c >>= 1) {
+            cfg.gridDim = dim3((unsigned)(a.n_chains * c), 1, 1);
+            attr[0].val.clusterDim.x = (unsigned)c;
+            int clusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&clusters, anneal_kernel<MODE>, &cfg) == cudaSuccess &&
+                clusters >= a.n_chains) {
+                cluster_size = c;
+                break;
+            }
+            cudaGetLastError();
+        }
+    }
+    cfg.gridDim = dim3((unsigned)(a.n_chains * cluster_size), 1, 1);
+    attr[0].val.clusterDim.x = (unsigned)cluster_size;
+    return cudaLaunchKernelEx(&cfg, anneal_kernel<MODE>, a);
+}
+
+cudaError_t launch_anneal(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
+    if (a.proposal == 0) return launch_mode<MODE_BEST_ALL>(a, cluster_size, st);
+    if (a.evaluate == 0) return launch_mode<MODE_UNIFORM_ALL>(a, cluster_size, st);
+    return launch_mode<MODE_UNIFORM_PROPOSAL>(a, cluster_size, st);
 }
 
 }  // namespace clv

@@ -529,8 +529,8 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
         (ap->proposal == 0 && ap->evaluate != 0))
         return fail(ctx, CLV_ERR_CARBON_SCHED, "invalid anneal parameters");
     if (n_params != 1 && n_params != n_chains) return fail(ctx, CLV_ERR_CARBON_SCHED, "n_params must be 1 or n_chains");
-    if (cluster_size != 1 && cluster_size != 2 && cluster_size != 4 && cluster_size != 8 && cluster_size != 16)
-        return fail(ctx, CLV_ERR_CARBON_SCHED, "cluster_size must be 1, 2, 4, 8 or 16");
+    if (cluster_size != 0 && cluster_size != 1 && cluster_size != 2 && cluster_size != 4 && cluster_size != 8 && cluster_size != 16)
+        return fail(ctx, CLV_ERR_CARBON_SCHED, "cluster_size must be 0 (auto), 1, 2, 4, 8 or 16");
     std::vector<EvalConst> ecs(n_params);
     for (int i = 0; i < n_params; ++i) {
         rc = make_ec(ctx, params + i, ctx->fam[family], ecs[i]);
