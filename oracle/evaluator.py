@@ -1,7 +1,9 @@
 """ORACLE -- TEST INFRASTRUCTURE ONLY.  The table-surrogate evaluator.
 
 Restates DESIGN.md "Scoring surrogate" (the replacement for SPEC:334-372's DES,
-SURVEY 7.2 D1) and SPEC-literal Eqs. 1, 2, 3, 6 in numpy.
+SURVEY 7.2 D1) and Eqs. 1, 2, 3, 6 in numpy.  Eq. 1 / Eq. 2 use
+the algebraically identical forms (A - A_base) * (100 / A_base) and
+100 - E * (ci / (10 C_base)); tests pin them to the SPEC-literal quotients.
 Aggregates are recomputed from scratch per candidate (W @ rows, int64), so this
 is independent of the device's incremental neighbour scoring.  Every fp64
 operation is one IEEE-rounded numpy ufunc in the documented order; the kernels
@@ -51,18 +53,20 @@ def epilogue(s_thr, s_acc, s_en, s_idle, lmax, tables, scenario) -> Evaluated:
     obj = scenario.obj
     a_base, c_base, slo = obj.base_accuracy, obj.base_carbon_g, obj.latency_slo_ms
     lam, ci = obj.carbon_weight, float(scenario.ci)
+    kA = 100.0 / a_base                       # Eq. 1 as (A - A_base) * kA
+    kC = ci / (10.0 * c_base)                 # Eq. 2 as 100 - E * kC
     with np.errstate(divide="ignore", invalid="ignore"):
-        thr_d = s_thr.astype(np.float64)
-        A = s_acc.astype(np.float64) / thr_d
-        rho = c["R_q"] / thr_d
-        e_act = (s_en.astype(np.float64) / thr_d) * c["en_scale"]
+        inv = 1.0 / s_thr.astype(np.float64)
+        A = s_acc.astype(np.float64) * inv
+        rho = c["R_q"] * inv
+        e_act = (s_en.astype(np.float64) * inv) * c["en_scale"]
         rho_c = np.minimum(rho, 1.0)
         p_idle = s_idle.astype(np.float64) * c["idle_scale"]
         E = e_act + ((1.0 - rho_c) * p_idle) * c["inv_3600R"]
         rho_q = np.minimum(rho, scenario.rho_sat)
         L = lmax / (1.0 - rho_q)
-        dA = (A - a_base) / a_base * 100.0
-        dC = (c_base - E / 1000.0 * ci) / c_base * 100.0
+        dA = (A - a_base) * kA
+        dC = 100.0 - E * kC
         f = lam * dC + (1.0 - lam) * dA
         sla = L <= slo
         soft = np.where((f >= 0) | bool(scenario.strict_eq6), -f * (slo / L), -f * (L / slo))

@@ -41,8 +41,11 @@ struct __align__(8) RemEnt {            // one removal multiset R (single edge o
     double d0, d1, d2, d3;                 // -(rows of R), exact integers
     unsigned long long mR;                 // presence mask (by latency rank) after removal
     int base;                              // canonical index of (R, A = {})
+    int off;                               // doubles: first entry of the static move list
+    int pre;                               // doubles: exclusive prefix of list lengths
     unsigned short code;                   // slice code of R: sr1*125 + sr2*25 (doubles), sr*5 (singles)
-    unsigned char r1, r2, c1, c2;          // removed edges and their neighbour counts
+    unsigned char r1, r2;                  // removed edges
+    int len;                               // doubles: move-list length
 };
 
 struct KRec {                              // (key, idx) record; payload hv in uniform mode
@@ -78,9 +81,6 @@ struct __align__(16) AnnealSmem {
     unsigned long long mem_ok;
     short Pt[CLV_MAX_EDGES + 1];           // P(x, y) = Pt[x] + y
     unsigned char sl[CLV_MAX_EDGES];
-    unsigned char nb_cnt[CLV_MAX_EDGES];
-    unsigned char nb[CLV_MAX_EDGES][CLV_NBMAX];
-    unsigned short ij_tab[CLV_NBMAX * CLV_NBMAX];
     unsigned short pair_tab[MAXP];
     // centre
     int w[CLV_MAX_EDGES];
@@ -90,8 +90,9 @@ struct __align__(16) AnnealSmem {
     // per-step tables
     RemEnt se[CLV_MAX_EDGES];
     RemEnt rp[MAXP];
-    int nPE, nRP;
+    int nPE, nRP, nLen;
     int warp_off[NWARP + 1];
+    int warp_len[NWARP + 1];
     unsigned char feasS[25];
     unsigned char feasD[625];
     // reduction
@@ -171,26 +172,38 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
 // present edges -- every CTA of the cluster must build identical tables because
 // the cluster partitions the move space by table position -- plus the
 // feasibility bytes of all 25 single / 625 double slice deltas.
-__device__ inline void prepare_step(AnnealSmem &s, int E, int n, const FeasView &F) {
+__device__ inline void prepare_step(AnnealSmem &s, const FamilyTables &T, int E, int n, const FeasView &F) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int NP = E * (E + 1) / 2;
-    int base = 0;
+    int base = 0, lbase = 0;
     for (int p0 = 0; p0 < NP; p0 += ANT) {
         const int p = p0 + threadIdx.x;
         bool ok = false;
-        int x = 0, y = 0;
+        int x = 0, y = 0, len = 0;
         if (p < NP) {
             x = s.pair_tab[p] & 0xFF; y = s.pair_tab[p] >> 8;
             const int wx = s.w[x], wy = s.w[y];
             ok = (x == y) ? (wx >= 2) : (wx > 0 && wy > 0);
+            if (ok) len = T.pair_len[p];
         }
         const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
+        int incl = len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y2 = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= d) incl += y2;
+        }
+        if (lane == 31) s.warp_len[wid] = incl;
         if (lane == 0) s.warp_off[wid] = __popc(bal);
         __syncthreads();
         if (threadIdx.x == 0) {
-            int acc = 0;
-            for (int q = 0; q < NWARP; ++q) { int c = s.warp_off[q]; s.warp_off[q] = acc; acc += c; }
-            s.warp_off[NWARP] = acc;
+            int acc = 0, lacc = 0;
+            for (int q = 0; q < NWARP; ++q) {
+                const int c = s.warp_off[q], l = s.warp_len[q];
+                s.warp_off[q] = acc; s.warp_len[q] = lacc;
+                acc += c; lacc += l;
+            }
+            s.warp_off[NWARP] = acc; s.warp_len[NWARP] = lacc;
         }
         __syncthreads();
         if (ok) {
@@ -207,11 +220,14 @@ __device__ inline void prepare_step(AnnealSmem &s, int E, int n, const FeasView 
             }
             r.mR = m;
             r.base = E * E + (s.Pt[x] + y) * NP;
+            r.off = T.pair_off[p];
+            r.len = len;
+            r.pre = lbase + s.warp_len[wid] + incl - len;
             r.code = (unsigned short)(s.sl[x] * 125 + s.sl[y] * 25);
             r.r1 = (unsigned char)x; r.r2 = (unsigned char)y;
-            r.c1 = s.nb_cnt[x]; r.c2 = s.nb_cnt[y];
         }
         base += s.warp_off[NWARP];
+        lbase += s.warp_len[NWARP];
         __syncthreads();
     }
     if (wid == 0) {
@@ -226,11 +242,11 @@ __device__ inline void prepare_step(AnnealSmem &s, int E, int n, const FeasView 
                 r.mR = (s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask;
                 r.base = e * E;
                 r.code = (unsigned short)(s.sl[e] * 5);
-                r.r1 = (unsigned char)e; r.r2 = 0xFF; r.c1 = 0; r.c2 = 0;
+                r.r1 = (unsigned char)e; r.r2 = 0xFF; r.off = 0; r.len = 0; r.pre = 0;
             }
             cnt += __popc(bal);
         }
-        if (lane == 0) { s.nPE = cnt; s.nRP = base; }
+        if (lane == 0) { s.nPE = cnt; s.nRP = base; s.nLen = lbase; }
     }
     for (int t = threadIdx.x; t < 650; t += ANT) {
         int v[CLV_K];
@@ -293,17 +309,12 @@ __global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ 
         s.lat_by_rank[e] = T.lat_by_rank[e];
         s.rbit[e] = 1ULL << T.rank[e];
         s.sl[e] = (unsigned char)(e % 5);
-        s.nb_cnt[e] = T.nb_cnt[e];
         unsigned long long am = 0;
         for (int x = 0; x < E; ++x)
             if (x != e && (x / 5 == e / 5 || x % 5 == e % 5)) am |= 1ULL << x;
         s.adjm[e] = am;
-        for (int k = 0; k < CLV_NBMAX; ++k) s.nb[e][k] = T.nb[e][k];
     }
     for (int x = tid; x <= E; x += ANT) s.Pt[x] = (short)(x * E - (x * (x - 1)) / 2 - x);
-    const int nbm = T.nbmax;
-    const int NB2 = nbm * nbm;
-    for (int t = tid; t < NB2; t += ANT) s.ij_tab[t] = (unsigned short)(((t / nbm) << 8) | (t % nbm));
     for (int x = tid; x < E; x += ANT)
         for (int y = x; y < E; ++y) s.pair_tab[x * E - (x * (x - 1)) / 2 + (y - x)] = (unsigned short)(x | (y << 8));
     if (tid == 0) {
@@ -360,7 +371,7 @@ __global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ 
     const unsigned long long mem_ok = s.mem_ok;
 
     for (int k = 0; !done; ++k) {
-        prepare_step(s, E, n, args.F);
+        prepare_step(s, T, E, n, args.F);
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
         unsigned long long cnt = 0;
         // ---- singles: (present edge i, target edge a)
@@ -382,33 +393,38 @@ __global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ 
                 if (a >= E) { a -= E; ++i; }
             }
         }
-        // ---- doubles: (removal pair j, neighbour slots ij)
+        // ---- doubles: (removal pair j, static move-list entry); warp-contiguous chunks
         {
-            const int nD = s.nRP * NB2;
-            int j = gt / NB2, ij = gt - (gt / NB2) * NB2;
-            const int dJ = G / NB2, dIJ = G - (G / NB2) * NB2;
-            for (int u = gt; u < nD; u += G) {
-                const RemEnt &R = s.rp[j];
-                const unsigned short tij = s.ij_tab[ij];
-                const int ii = tij >> 8, jj = tij & 0xFF;
-                bool ok = ii < R.c1 && jj < R.c2;
-                if (ok) {
-                    const int a1 = s.nb[R.r1][ii], a2 = s.nb[R.r2][jj];
-                    ok = a1 != R.r2 && a2 != R.r1 &&
-                         !(a1 > a2 && ((s.adjm[R.r1] >> a2) & 1ULL) && ((s.adjm[R.r2] >> a1) & 1ULL)) &&
-                         s.feasD[R.code + s.sl[a1] * 5 + s.sl[a2]];
-                    if (ok) {
+            const int lane = tid & 31, wid = tid >> 5;
+            const int ND = s.nLen;
+            const int W = CL * NWARP;
+            const int chunk = (((ND + W - 1) / W) + 31) & ~31;
+            const int gw = crank * NWARP + wid;
+            int t = gw * chunk + lane;
+            const int tend = min(gw * chunk + chunk, ND);
+            if (gw * chunk < ND) {
+                int lo = 0, hi = s.nRP - 1;
+                const int t0 = t < ND ? t : ND - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s.rp[mid].pre <= t0) lo = mid; else hi = mid - 1;
+                }
+                int j = lo;
+                const uint32_t *plist = T.pair_list;
+                for (; t < tend; t += 32) {
+                    while (t >= s.rp[j].pre + s.rp[j].len) ++j;
+                    const RemEnt &R = s.rp[j];
+                    const uint32_t ent = __ldg(plist + R.off + (t - R.pre));
+                    if (s.feasD[R.code + ((ent >> 12) & 31)]) {
                         ++cnt;
+                        const int a1 = ent & 63, a2 = (ent >> 6) & 63;
                         const ARow &A1 = s.row[a1], &A2 = s.row[a2];
-                        const int lo = a1 < a2 ? a1 : a2, hi = a1 < a2 ? a2 : a1;
                         fold<MODE>(s, s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
                                    s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
-                                   R.mR | s.rbit[a1] | s.rbit[a2], (long long)(R.base + s.Pt[lo] + hi),
+                                   R.mR | s.rbit[a1] | s.rbit[a2], (long long)(R.base + (int)(ent >> 17)),
                                    rS, rV, rP, args.seed, gchain, (uint64_t)k);
                     }
                 }
-                j += dJ; ij += dIJ;
-                if (ij >= NB2) { ij -= NB2; ++j; }
             }
         }
         // ---- CTA reduction, then DSMEM publish into the leader's slots
@@ -575,7 +591,7 @@ static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream
     if (cluster_size <= 0) {
         // Largest cluster size that still keeps every chain resident (one wave).
         cluster_size = 1;
-        for (int c = 16; c >= 2; c >>= 1) {
+        for (int c = MAXCL; c >= 2; --c) {
             cfg.gridDim = dim3((unsigned)(a.n_chains * c), 1, 1);
             attr[0].val.clusterDim.x = (unsigned)c;
             int clusters = 0;

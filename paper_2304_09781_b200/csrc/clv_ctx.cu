@@ -20,6 +20,7 @@ struct clv_ctx {
     Topology *topo_dev = nullptr;
     bool fam_set[CLV_MAX_FAMILIES] = {};
     FamilyTables fam[CLV_MAX_FAMILIES];
+    uint32_t *pair_list_dev[CLV_MAX_FAMILIES] = {};
     FamilyTables *fam_dev = nullptr;
     // feasibility tables
     int feas_nmax = -1;
@@ -89,6 +90,8 @@ int make_ec(clv_ctx *ctx, const clv_eval_params *p, const FamilyTables &T, EvalC
     ec.slo = p->latency_slo_ms;
     ec.ci = p->ci;
     ec.lam = std::min(1.0, std::max(0.0, p->carbon_weight));
+    ec.kA = 100.0 / p->base_accuracy;
+    ec.kC = p->ci / (10.0 * p->base_carbon_g);
     ec.strict = p->strict_eq6 ? 1 : 0;
     ec.n = p->n_gpus;
     return CLV_OK;
@@ -197,6 +200,7 @@ void clv_destroy(clv_ctx *ctx) {
     cudaFreeHost(ctx->host_rec); cudaFreeHost(ctx->host_cnt);
     cudaFree(ctx->err_flag); cudaFree(ctx->err_index); cudaFreeHost(ctx->host_err);
     cudaFree(ctx->ec_dev); cudaFree(ctx->small_dev);
+    for (int f = 0; f < CLV_MAX_FAMILIES; ++f) cudaFree(ctx->pair_list_dev[f]);
     delete ctx;
 }
 
@@ -298,7 +302,35 @@ int clv_set_profile(clv_ctx *ctx, int family, int V, const int64_t *thr_q, const
             if ((T.mem_ok >> (v * 5 + k)) & 1ULL) T.feas_list[k][c++] = (unsigned char)v;
         T.nfeas[k] = (unsigned char)c;
     }
+    // static double-move lists (see FamilyTables::pair_list)
+    std::vector<uint32_t> plist;
+    auto adj = [](int x, int y) { return x != y && (x / 5 == y / 5 || x % 5 == y % 5); };
+    auto P = [&](int x, int y) { return x * T.E - (x * (x - 1)) / 2 + (y - x); };
+    for (int r1 = 0; r1 < T.E; ++r1)
+        for (int r2 = r1; r2 < T.E; ++r2) {
+            const int p = P(r1, r2);
+            T.pair_off[p] = (int)plist.size();
+            int len = 0;
+            for (int ii = 0; ii < T.nb_cnt[r1]; ++ii)
+                for (int jj = 0; jj < T.nb_cnt[r2]; ++jj) {
+                    const int a1 = T.nb[r1][ii], a2 = T.nb[r2][jj];
+                    if (a1 == r2 || a2 == r1) continue;
+                    if (a1 > a2 && adj(r1, a2) && adj(r2, a1)) continue;
+                    const int lo = std::min(a1, a2), hi = std::max(a1, a2);
+                    plist.push_back((uint32_t)a1 | ((uint32_t)a2 << 6) |
+                                    ((uint32_t)((a1 % 5) * 5 + (a2 % 5)) << 12) | ((uint32_t)P(lo, hi) << 17));
+                    ++len;
+                }
+            if (len > 255) return fail(ctx, CLV_ERR_PROFILE, "internal: move list too long");
+            T.pair_len[p] = (unsigned char)len;
+        }
     CLV_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaFree(ctx->pair_list_dev[family]);
+    ctx->pair_list_dev[family] = nullptr;
+    CLV_CUDA(cudaMalloc(&ctx->pair_list_dev[family], std::max<size_t>(1, plist.size()) * sizeof(uint32_t)), "alloc move lists");
+    if (!plist.empty())
+        CLV_CUDA(cudaMemcpy(ctx->pair_list_dev[family], plist.data(), plist.size() * sizeof(uint32_t), cudaMemcpyHostToDevice), "copy move lists");
+    T.pair_list = ctx->pair_list_dev[family];
     CLV_CUDA(cudaMemcpy(ctx->fam_dev + family, &T, sizeof(FamilyTables), cudaMemcpyHostToDevice), "copy profile");
     ctx->fam[family] = T;
     ctx->fam_set[family] = true;
@@ -529,8 +561,8 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
         (ap->proposal == 0 && ap->evaluate != 0))
         return fail(ctx, CLV_ERR_CARBON_SCHED, "invalid anneal parameters");
     if (n_params != 1 && n_params != n_chains) return fail(ctx, CLV_ERR_CARBON_SCHED, "n_params must be 1 or n_chains");
-    if (cluster_size != 0 && cluster_size != 1 && cluster_size != 2 && cluster_size != 4 && cluster_size != 8 && cluster_size != 16)
-        return fail(ctx, CLV_ERR_CARBON_SCHED, "cluster_size must be 0 (auto), 1, 2, 4, 8 or 16");
+    if (cluster_size < 0 || cluster_size > 16)
+        return fail(ctx, CLV_ERR_CARBON_SCHED, "cluster_size must be 0 (auto) or 1..16");
     std::vector<EvalConst> ecs(n_params);
     for (int i = 0; i < n_params; ++i) {
         rc = make_ec(ctx, params + i, ctx->fam[family], ecs[i]);

@@ -118,7 +118,7 @@ def test_oracle_search_c0(engine):
     assert got["sla_count"] == int(ev.sla.sum())
 
 
-def _chain_compare(engine, prof, T, starts, scs, ap, seed, n, feas, cluster=4):
+def _chain_compare(engine, prof, T, starts, scs, ap, seed, n, feas, cluster=0):
     batch = engine.anneal(starts, prof, scs, ap, seed, n=n, cluster=cluster, log=True)
     host = batch.host()
     for c in range(len(starts)):
