@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--workload", default="c2", choices=["c0", "c1", "c2", "c4"],
+                    help="c2 (default) is the headline; c0/c1/c4 are the other BASELINE configs")
+    ap.add_argument("--sweep", type=int, default=1_000_000_000, help="c4: candidates per sweep (whole job)")
     return ap.parse_args()
 
 
@@ -260,6 +263,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.workload != "c2":
+        return run_other(args, rank, world, local)
     from paper_2304_09781_b200.engine import CloverEngine, RECORD_DTYPE
     from paper_2304_09781_b200.profiles import synthetic_profile
     from paper_2304_09781_b200.search import anneal_chains, exchange_record
@@ -388,6 +393,91 @@ def main():
             "chain_steps_per_replan": chain_steps_all / args.steps,
             "wall_s_timed_region": t_wall}
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------- the other BASELINE configs
+def _timed_steps(fn, steps, warmup, flush):
+    import torch
+    ev = []
+    for s in range(warmup + steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = fn(s)
+        e1.record()
+        ev.append((e0, e1, out))
+    torch.cuda.synchronize()
+    return [(a.elapsed_time(b), o) for a, b, o in ev[warmup:]]
+
+
+def run_other(args, rank, world, local):
+    """c0 (ORACLE, n=1), c1 (lambda sweep, n=8), c4 (10^9 two-pod sweep, n=256)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2304_09781_b200.engine import CloverEngine
+    from paper_2304_09781_b200.profiles import synthetic_profile
+    from paper_2304_09781_b200.distributed import shard
+    from paper_2304_09781_b200.search import exchange_record
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    eng = CloverEngine(device=local)
+    extra = {}
+    if args.workload == "c0":
+        prof = synthetic_profile("efficientnet")
+        sc = eng.calibrate(prof, 1, 400.0, 0.5)
+        total = eng.oracle_size(prof)
+        b, e = shard(total, rank, world)
+        res = _timed_steps(lambda s: eng.oracle_search(prof, sc, b, e), args.steps, args.warmup, flush)
+        per_step = [r[1]["valid_count"] for r in res]
+        cfg = "c0: n=1 GPU, EfficientNet B1-B7 (V=7), lambda=0.5, ci=400, exhaustive standardized ORACLE " \
+              "(%d candidates, sharded by index range)" % total
+        extra["winner"] = eng.oracle_decode(prof, res[-1][1]["index"])
+        scaling = "strong"
+    elif args.workload == "c1":
+        prof = synthetic_profile("efficientnet")
+        n = 8
+        eng.build_feasibility(n)
+        lams = [i / 10 for i in range(11)]
+        scs = [eng.calibrate(prof, n, 400.0, l) for l in lams]
+        from paper_2304_09781_b200.objective import AnnealParams
+        ap = AnnealParams(max_steps=args.max_steps)
+        V = prof.variant_count
+        start = np.zeros((len(lams), V * 5), dtype=np.uint16)
+        start[:, (V - 1) * 5] = n
+        sd = torch.from_numpy(start.view(np.int16)).cuda().view(torch.uint16)
+        def step(s):
+            b = eng.anneal(sd, prof, scs, ap, SEED + s, chain_base=rank * len(lams))
+            exchange_record(eng, eng.select_chains(b))
+            return b
+        res = _timed_steps(step, args.steps, args.warmup, flush)
+        per_step = [int(r[1].host()["results"]["evals"].sum()) for r in res]
+        cfg = "c1: n=8 GPUs, EfficientNet B1-B7 (V=7), lambda sweep 0..1 (11 chains from BASE, one per lambda), " \
+              "full GED<=4 neighbourhood per step, to termination; replicas across GPUs"
+        scaling = "weak"
+    else:
+        pr, pb = synthetic_profile("resnet"), synthetic_profile("bert")
+        sr, sb = eng.calibrate(pr, 128, 300.0, 0.5), eng.calibrate(pb, 128, 300.0, 0.5)
+        pods = [(pr, sr, 128, 0.5), (pb, sb, 128, 0.5)]
+        b, e = shard(args.sweep, rank, world)
+        res = _timed_steps(lambda s: eng.sweep(pods, b, e, SEED + s), args.steps, args.warmup, flush)
+        per_step = [r[1]["valid_count"] for r in res]
+        cfg = "c4: n=256 GPUs as two 128-GPU pods (ResNet V=5 | BERT V=6), counter-RNG x-space sweep of %d " \
+              "candidates per step (sharded by index range)" % args.sweep
+        scaling = "strong"
+    ms = [r[0] for r in res]
+    t = torch.tensor([sum(ms) / 1000.0, float(sum(per_step))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        a = t[0:1].clone(); dist.all_reduce(a, op=dist.ReduceOp.MAX)
+        c = t[1:2].clone(); dist.all_reduce(c)
+        t = torch.cat([a, c])
+    if rank == 0:
+        line = {"metric": METRIC, "value": t[1].item() / t[0].item(), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t[0].item() / args.steps,
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": cfg}, "candidates_per_step": t[1].item() / args.steps}
+        line.update({k: str(v) for k, v in extra.items()})
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

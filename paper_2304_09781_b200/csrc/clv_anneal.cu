@@ -93,6 +93,7 @@ struct __align__(16) AnnealSmem {
     int nPE, nRP, nLen;
     int warp_off[NWARP + 1];
     int warp_len[NWARP + 1];
+    int fsvec[CLV_K];                      // slice vector the feasibility bytes belong to
     unsigned char feasS[25];
     unsigned char feasD[625];
     // reduction
@@ -117,14 +118,10 @@ __device__ inline void decode_move(const AnnealSmem &s, int E, long long idx, in
         return;
     }
     const int NP = E * (E + 1) / 2;
-    long long u = idx - (long long)E * E;
-    int p = (int)(u / NP), q = (int)(u % NP);
-    int x = 0;
-    while (x + 1 < E && s.Pt[x + 1] + x + 1 <= p) ++x;
-    r1 = x; r2 = p - s.Pt[x];
-    x = 0;
-    while (x + 1 < E && s.Pt[x + 1] + x + 1 <= q) ++x;
-    a1 = x; a2 = q - s.Pt[x];
+    const long long u = idx - (long long)E * E;
+    const int p = (int)(u / NP), q = (int)(u - (long long)p * NP);
+    r1 = s.pair_tab[p] & 0xFF; r2 = s.pair_tab[p] >> 8;
+    a1 = s.pair_tab[q] & 0xFF; a2 = s.pair_tab[q] >> 8;
 }
 
 __device__ inline Score score_move(const AnnealSmem &s, int r1, int r2, int a1, int a2) {
@@ -175,94 +172,103 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
 __device__ inline void prepare_step(AnnealSmem &s, const FamilyTables &T, int E, int n, const FeasView &F) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int NP = E * (E + 1) / 2;
-    int base = 0, lbase = 0;
-    for (int p0 = 0; p0 < NP; p0 += ANT) {
-        const int p = p0 + threadIdx.x;
-        bool ok = false;
-        int x = 0, y = 0, len = 0;
-        if (p < NP) {
-            x = s.pair_tab[p] & 0xFF; y = s.pair_tab[p] >> 8;
-            const int wx = s.w[x], wy = s.w[y];
-            ok = (x == y) ? (wx >= 2) : (wx > 0 && wy > 0);
-            if (ok) len = T.pair_len[p];
-        }
-        const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
-        int incl = len;
+    const int PER = (NP + ANT - 1) / ANT;          // consecutive pairs per thread (<= 4)
+    const int p0 = threadIdx.x * PER;
+    int cnt = 0, lsum = 0;
+    for (int p = p0; p < p0 + PER && p < NP; ++p) {
+        const int x = s.pair_tab[p] & 0xFF, y = s.pair_tab[p] >> 8;
+        const bool ok = (x == y) ? (s.w[x] >= 2) : (s.w[x] > 0 && s.w[y] > 0);
+        if (ok) { ++cnt; lsum += T.pair_len[p]; }
+    }
+    // block exclusive scan of (cnt, lsum) in thread order
+    int ic = cnt, il = lsum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int yc = __shfl_up_sync(0xFFFFFFFFu, ic, d), yl = __shfl_up_sync(0xFFFFFFFFu, il, d);
+        if (lane >= d) { ic += yc; il += yl; }
+    }
+    if (lane == 31) { s.warp_off[wid] = ic; s.warp_len[wid] = il; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int c = lane < NWARP ? s.warp_off[lane] : 0, l = lane < NWARP ? s.warp_len[lane] : 0;
+        int c2 = c, l2 = l;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const int y2 = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-            if (lane >= d) incl += y2;
+            const int yc = __shfl_up_sync(0xFFFFFFFFu, c2, d), yl = __shfl_up_sync(0xFFFFFFFFu, l2, d);
+            if (lane >= d) { c2 += yc; l2 += yl; }
         }
-        if (lane == 31) s.warp_len[wid] = incl;
-        if (lane == 0) s.warp_off[wid] = __popc(bal);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int acc = 0, lacc = 0;
-            for (int q = 0; q < NWARP; ++q) {
-                const int c = s.warp_off[q], l = s.warp_len[q];
-                s.warp_off[q] = acc; s.warp_len[q] = lacc;
-                acc += c; lacc += l;
-            }
-            s.warp_off[NWARP] = acc; s.warp_len[NWARP] = lacc;
+        if (lane < NWARP) { s.warp_off[lane] = c2 - c; s.warp_len[lane] = l2 - l; }
+        if (lane == NWARP - 1) { s.nRP = c2; s.nLen = l2; }
+    }
+    __syncthreads();
+    int pos = s.warp_off[wid] + ic - cnt, lpos = s.warp_len[wid] + il - lsum;
+    for (int p = p0; p < p0 + PER && p < NP; ++p) {
+        const int x = s.pair_tab[p] & 0xFF, y = s.pair_tab[p] >> 8;
+        const bool ok = (x == y) ? (s.w[x] >= 2) : (s.w[x] > 0 && s.w[y] > 0);
+        if (!ok) continue;
+        RemEnt &r = s.rp[pos++];
+        r.d0 = -(s.row[x].thr + s.row[y].thr);
+        r.d1 = -(s.row[x].acc + s.row[y].acc);
+        r.d2 = -(s.row[x].en + s.row[y].en);
+        r.d3 = -(s.row[x].idle + s.row[y].idle);
+        unsigned long long m = s.pmask;
+        if (x == y) { if (s.w[x] == 2) m &= ~s.rbit[x]; }
+        else {
+            if (s.w[x] == 1) m &= ~s.rbit[x];
+            if (s.w[y] == 1) m &= ~s.rbit[y];
         }
-        __syncthreads();
-        if (ok) {
-            RemEnt &r = s.rp[base + s.warp_off[wid] + __popc(bal & ((1u << lane) - 1u))];
-            r.d0 = -(s.row[x].thr + s.row[y].thr);
-            r.d1 = -(s.row[x].acc + s.row[y].acc);
-            r.d2 = -(s.row[x].en + s.row[y].en);
-            r.d3 = -(s.row[x].idle + s.row[y].idle);
-            unsigned long long m = s.pmask;
-            if (x == y) { if (s.w[x] == 2) m &= ~s.rbit[x]; }
-            else {
-                if (s.w[x] == 1) m &= ~s.rbit[x];
-                if (s.w[y] == 1) m &= ~s.rbit[y];
-            }
-            r.mR = m;
-            r.base = E * E + (s.Pt[x] + y) * NP;
-            r.off = T.pair_off[p];
-            r.len = len;
-            r.pre = lbase + s.warp_len[wid] + incl - len;
-            r.code = (unsigned short)(s.sl[x] * 125 + s.sl[y] * 25);
-            r.r1 = (unsigned char)x; r.r2 = (unsigned char)y;
-        }
-        base += s.warp_off[NWARP];
-        lbase += s.warp_len[NWARP];
-        __syncthreads();
+        r.mR = m;
+        r.base = E * E + p * NP;
+        r.off = T.pair_off[p];
+        r.len = T.pair_len[p];
+        r.pre = lpos;
+        lpos += r.len;
+        r.code = (unsigned short)(s.sl[x] * 125 + s.sl[y] * 25);
+        r.r1 = (unsigned char)x; r.r2 = (unsigned char)y;
     }
     if (wid == 0) {
-        int cnt = 0;
+        int c = 0;
         for (int e0 = 0; e0 < E; e0 += 32) {
             const int e = e0 + lane;
             const bool ok = e < E && s.w[e] > 0;
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
             if (ok) {
-                RemEnt &r = s.se[cnt + __popc(bal & ((1u << lane) - 1u))];
+                RemEnt &r = s.se[c + __popc(bal & ((1u << lane) - 1u))];
                 r.d0 = -s.row[e].thr; r.d1 = -s.row[e].acc; r.d2 = -s.row[e].en; r.d3 = -s.row[e].idle;
                 r.mR = (s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask;
                 r.base = e * E;
                 r.code = (unsigned short)(s.sl[e] * 5);
                 r.r1 = (unsigned char)e; r.r2 = 0xFF; r.off = 0; r.len = 0; r.pre = 0;
             }
-            cnt += __popc(bal);
+            c += __popc(bal);
         }
-        if (lane == 0) { s.nPE = cnt; s.nRP = base; s.nLen = lbase; }
+        if (lane == 0) s.nPE = c;
     }
-    for (int t = threadIdx.x; t < 650; t += ANT) {
-        int v[CLV_K];
+    // slice-delta feasibility: only when the centre's slice multiset changed
+    // (variant swaps keep it), the cache stays valid
+    bool same = true;
 #pragma unroll
-        for (int k = 0; k < CLV_K; ++k) v[k] = s.svec[k];
-        if (t < 25) {
-            v[t / 5] -= 1; v[t % 5] += 1;
-            s.feasS[t] = v[t / 5] >= 0 && feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
-        } else {
-            const int u = t - 25;
-            v[u / 125] -= 1; v[(u / 25) % 5] -= 1; v[(u / 5) % 5] += 1; v[u % 5] += 1;
-            s.feasD[u] = v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[3] >= 0 && v[4] >= 0 &&
-                         feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
-        }
-    }
+    for (int k = 0; k < CLV_K; ++k) same &= (s.svec[k] == s.fsvec[k]);
     __syncthreads();
+    if (!same) {
+        for (int t = threadIdx.x; t < 650; t += ANT) {
+            int v[CLV_K];
+#pragma unroll
+            for (int k = 0; k < CLV_K; ++k) v[k] = s.svec[k];
+            if (t < 25) {
+                v[t / 5] -= 1; v[t % 5] += 1;
+                s.feasS[t] = v[t / 5] >= 0 && feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
+            } else {
+                const int u = t - 25;
+                v[u / 125] -= 1; v[(u / 25) % 5] -= 1; v[(u / 5) % 5] += 1; v[u % 5] += 1;
+                s.feasD[u] = v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[3] >= 0 && v[4] >= 0 &&
+                             feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < CLV_K) s.fsvec[threadIdx.x] = s.svec[threadIdx.x];
+        __syncthreads();
+    }
 }
 
 // Fold one valid neighbour into the thread's records.
@@ -336,6 +342,7 @@ __global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ 
         }
         s.S[0] = S0; s.S[1] = S1; s.S[2] = S2; s.S[3] = S3;
         s.pmask = m;
+        for (int k = 0; k < CLV_K; ++k) s.fsvec[k] = -1;
     }
     __syncthreads();
 
