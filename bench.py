@@ -461,7 +461,7 @@ def run_other(args, rank, world, local):
         pods = [(pr, sr, 128, 0.5), (pb, sb, 128, 0.5)]
         b, e = shard(args.sweep, rank, world)
         res = _timed_steps(lambda s: eng.sweep(pods, b, e, SEED + s), args.steps, args.warmup, flush)
-        per_step = [r[1]["valid_count"] for r in res]
+        per_step = [r[1][0]["valid_count"] for r in res]
         cfg = "c4: n=256 GPUs as two 128-GPU pods (ResNet V=5 | BERT V=6), counter-RNG x-space sweep of %d " \
               "candidates per step (sharded by index range)" % args.sweep
         scaling = "strong"
