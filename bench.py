@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--workload", default="c2", choices=["c0", "c1", "c2", "c4"],
+    ap.add_argument("--workload", default="c2", choices=["c0", "c1", "c2", "c3", "c4"],
                     help="c2 (default) is the headline; c0/c1/c4 are the other BASELINE configs")
     ap.add_argument("--sweep", type=int, default=1_000_000_000, help="c4: candidates per sweep (whole job)")
     return ap.parse_args()
@@ -260,9 +260,14 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    backend = os.environ.get("CLV_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     if args.workload != "c2":
         return run_other(args, rank, world, local)
     from paper_2304_09781_b200.engine import CloverEngine, RECORD_DTYPE
@@ -333,8 +338,9 @@ def main():
     evals = sum(int(batches[s].host()["results"]["evals"].sum()) for s in range(args.warmup, total_steps))
     chain_steps = sum(int(batches[s].host()["results"]["steps"].sum()) for s in range(args.warmup, total_steps))
     dev_time = sum(step_ms) / 1000.0
+    rdev = "cuda" if backend == "nccl" else "cpu"
     t = torch.tensor([dev_time, float(evals), sum(anneal_ms) / 1000.0, float(chain_steps)], dtype=torch.float64,
-                     device="cuda")
+                     device=rdev)
     if world > 1:
         tmax = t.clone(); dist.all_reduce(tmax[0:1], op=dist.ReduceOp.MAX); dist.all_reduce(tmax[2:3], op=dist.ReduceOp.MAX)
         tsum = t.clone(); dist.all_reduce(tsum[1:2]); dist.all_reduce(tsum[3:4])
@@ -354,7 +360,7 @@ def main():
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
         e2e_evals += res.evals
-    et = torch.tensor([sum(e2e_times), float(e2e_evals)], dtype=torch.float64, device="cuda")
+    et = torch.tensor([sum(e2e_times), float(e2e_evals)], dtype=torch.float64, device=rdev)
     if world > 1:
         a = et[0:1].clone(); dist.all_reduce(a, op=dist.ReduceOp.MAX)
         b = et[1:2].clone(); dist.all_reduce(b)
@@ -434,6 +440,26 @@ def run_other(args, rank, world, local):
               "(%d candidates, sharded by index range)" % total
         extra["winner"] = eng.oracle_decode(prof, res[-1][1]["index"])
         scaling = "strong"
+    elif args.workload == "c3":
+        from paper_2304_09781_b200.controller import run_trace, ControllerParams
+        from paper_2304_09781_b200.objective import AnnealParams
+        from paper_2304_09781_b200.profiles import synthetic_trace
+        prof = synthetic_profile("efficientnet")
+        eng.build_feasibility(N_FLEET)
+        tr = synthetic_trace(hours=24.0)
+        ap = AnnealParams(proposal="uniform", evaluate="all", max_steps=args.max_steps)
+        rep = run_trace(eng, tr, "clover", N_FLEET, prof, LAMBDA, ap, ControllerParams(), seed=SEED,
+                        chains=args.chains, chain_base=rank * args.chains)
+        res = [(r.device_ms, r.evals) for r in rep.replans]
+        per_step = [e for _, e in res]
+        cfg = "c3: 24 h synthetic ci trace (288 ticks at 5 min), re-plan when |dci|/ci > 5%% from the incumbent, " \
+              "strict p95 SLA, n=%d GPUs, %d chains per B200 (uniform proposal, full neighbourhood), " \
+              "one step = one re-plan" % (N_FLEET, args.chains)
+        extra["summary"] = json.dumps(rep.summary)
+        extra["replan_device_ms"] = json.dumps([round(r.device_ms, 3) for r in rep.replans])
+        scaling = "weak"
+        args.steps = len(res)
+        res = [(ms, None) for ms, _ in res]
     elif args.workload == "c1":
         prof = synthetic_profile("efficientnet")
         n = 8
@@ -466,7 +492,8 @@ def run_other(args, rank, world, local):
               "candidates per step (sharded by index range)" % args.sweep
         scaling = "strong"
     ms = [r[0] for r in res]
-    t = torch.tensor([sum(ms) / 1000.0, float(sum(per_step))], dtype=torch.float64, device="cuda")
+    t = torch.tensor([sum(ms) / 1000.0, float(sum(per_step))], dtype=torch.float64,
+                     device="cuda" if os.environ.get("CLV_DIST_BACKEND", "nccl") == "nccl" else "cpu")
     if world > 1:
         a = t[0:1].clone(); dist.all_reduce(a, op=dist.ReduceOp.MAX)
         c = t[1:2].clone(); dist.all_reduce(c)

@@ -1,0 +1,197 @@
+"""Trace-driven re-planning controller (BASELINE configs[3]).
+
+``run_trace`` ticks through a carbon-intensity trace every ``trace_step_s``; when
+``reopt_needed`` fires (|Δci|/ci > 5 %) it re-plans with
+the chosen scheme starting from the incumbent, seeded by
+``derive_seed(seed, tick)``, keeps the incumbent unless the result
+meets the p95 SLA (strict SLA), diffs the realized FleetConfigs for the
+reconfiguration downtime and accrues carbon between ticks
+(× PUE).  Every re-plan's time-to-solution is recorded (device time
+of the search launch + winner exchange, and host wall time including realize).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field, replace
+from typing import Optional
+
+import numpy as np
+
+from .core import derive_seed
+from .engine import CloverEngine
+from .errors import CarbonSchedError
+from .graph import ConfigGraph, build_graph
+from .objective import AnnealParams, Scenario
+from .profiles import CarbonTrace, ProfileTable, intensity_at
+
+SCHEMES = ("base", "co2opt", "blover", "clover", "oracle")
+
+
+@dataclass(frozen=True)
+class ControllerParams:
+    """SPEC:569-572."""
+
+    reopt_threshold: float = 0.05
+    reconfig_downtime_s: float = 30.0
+    trace_step_s: float = 300.0
+
+    def __post_init__(self):
+        if not self.reopt_threshold > 0 or self.reconfig_downtime_s < 0 or not self.trace_step_s > 0:
+            raise CarbonSchedError("invalid controller parameters")
+
+
+def reopt_needed(prev_ci: float, ci: float, p: ControllerParams = ControllerParams()) -> bool:
+    """|ci - prev| / prev > threshold; prev = 0 always re-optimises."""
+    if prev_ci <= 0:
+        return True
+    return abs(ci - prev_ci) / prev_ci > p.reopt_threshold
+
+
+@dataclass
+class Replan:
+    tick: int
+    t: float
+    ci: float
+    prev_ci: float
+    device_ms: float
+    wall_ms: float
+    evals: int
+    accepted: bool
+    f: float
+    h: float
+    p95_ms: float
+    sla_met: bool
+    changed_gpus: int
+
+
+@dataclass
+class TimelineReport:
+    rows: list = field(default_factory=list)
+    replans: list = field(default_factory=list)
+    summary: dict = field(default_factory=dict)
+
+
+def _score(engine, profile, w, scenario):
+    best, _ = engine.score_graphs(np.asarray(w, dtype=np.uint16)[None, :], profile, scenario, outputs=False)
+    if not best["found"]:
+        raise CarbonSchedError("active configuration is not realizable")
+    return best
+
+
+def _changed_gpus(a, b) -> int:
+    """GPUs whose partition or any assignment differs between two realized fleets."""
+    if a is None:
+        return len(b.partitions)
+    ga, gb = a.instances(), b.instances()
+    per_a = {}
+    for g, s, v in ga:
+        per_a.setdefault(g, []).append((int(s), v))
+    per_b = {}
+    for g, s, v in gb:
+        per_b.setdefault(g, []).append((int(s), v))
+    return sum(1 for g in range(len(b.partitions)) if per_a.get(g) != per_b.get(g))
+
+
+def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, profile: ProfileTable,
+              lam: float = 0.5, ap: Optional[AnnealParams] = None, cp: ControllerParams = ControllerParams(),
+              seed: int = 0, chains: int = 128, utilization: float = 0.7, strict_sla: bool = True,
+              pue: float = 1.5, chain_base: int = 0, group=None) -> TimelineReport:
+    """Trace-driven control loop for ``scheme`` in SCHEMES."""
+    import torch
+    from .search import anneal_chains, base_config, co2opt_config
+    if scheme not in SCHEMES:
+        raise CarbonSchedError("unknown scheme %r" % scheme)
+    ap = ap or AnnealParams(proposal="uniform", evaluate="all", max_steps=64)
+    ci_mean = trace.mean()
+    # L_tail and C_base from BASE at the trace's mean intensity (D7)
+    base_sc = engine.calibrate(profile, n, ci_mean, lam, utilization, ci_base=ci_mean, pue=pue)
+    base_w = np.array(build_graph(base_config(n, profile), profile).weights, dtype=np.int64)
+    if scheme == "co2opt":
+        w = np.array(build_graph(co2opt_config(n, profile), profile).weights, dtype=np.int64)
+    else:
+        w = base_w.copy()
+    fleet = engine.realize(ConfigGraph(w, profile.variant_count, profile.name), n)
+    rep = TimelineReport()
+    prev_ci = 0.0
+    cum, cum_base, acc_sum = 0.0, 0.0, 0.0
+    steps = int(round((trace.samples[-1][0] - trace.samples[0][0]) / cp.trace_step_s)) + 1
+    t0 = trace.samples[0][0]
+    for tick in range(steps):
+        t = t0 + tick * cp.trace_step_s
+        ci = intensity_at(trace, t)
+        sc = base_sc.with_ci(ci)
+        optimizing = False
+        if scheme in ("clover", "oracle", "blover") and reopt_needed(prev_ci, ci, cp):
+            optimizing = True
+            tick_seed = derive_seed(seed, tick)
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            if scheme == "clover":
+                starts = np.repeat(w[None, :].astype(np.uint16), chains, axis=0)
+                res = anneal_chains(engine, starts, profile, sc, ap, tick_seed, chain_base=chain_base,
+                                    group=group)
+                cand_w = np.asarray(res.best.graph.weights, dtype=np.int64)
+                cand = dict(f=res.best.f_value, h=res.best.h_value, p95_ms=res.best.p95_ms,
+                            sla_met=res.best.sla_met)
+                evals = res.evals
+            elif scheme == "oracle":
+                o = engine.oracle_search(profile, sc)
+                cid, assign = engine.oracle_decode(profile, o["index"])
+                from .mig import FleetConfig
+                fc = FleetConfig([cid] * n, list(assign) * n, profile.topology)
+                cand_w = np.array(build_graph(fc, profile).weights, dtype=np.int64)
+                cand = dict(f=o["f"], h=o["h"], p95_ms=o["p95_ms"], sla_met=bool(o["sla_met"]))
+                evals = o["valid_count"]
+            else:
+                budget = max(1, math.ceil(ap.time_budget_s / ap.eval_cost_s))
+                best, _ = engine.sweep([(profile, sc, n, 1.0)], 0, budget, tick_seed)
+                fc = engine.sweep_decode([(profile, sc, n, 1.0)], tick_seed, best["index"])[0]
+                cand_w = np.array(build_graph(fc, profile).weights, dtype=np.int64)
+                cand = dict(f=best["f"], h=best["h"], p95_ms=0.0, sla_met=bool(best["sla_met"]))
+                evals = best["valid_count"]
+            e1.record()
+            torch.cuda.synchronize()
+            dev_ms = e0.elapsed_time(e1)
+            cur = _score(engine, profile, w, sc)
+            better = (cand["sla_met"] and not cur["sla_met"]) or \
+                     (cand["sla_met"] == bool(cur["sla_met"]) and cand["h"] < cur["h"])
+            accepted = bool(better and (cand["sla_met"] or not strict_sla))
+            changed = 0
+            if accepted:
+                new_fleet = engine.realize(ConfigGraph(cand_w, profile.variant_count, profile.name), n)
+                changed = _changed_gpus(fleet, new_fleet)
+                fleet, w = new_fleet, cand_w
+            wall_ms = 1000.0 * (time.perf_counter() - w0)
+            rep.replans.append(Replan(tick, t, ci, prev_ci, dev_ms, wall_ms, int(evals), accepted, cand["f"],
+                                      cand["h"], cand["p95_ms"], bool(cand["sla_met"]), changed))
+            prev_ci = ci
+        elif prev_ci <= 0:
+            prev_ci = ci
+        act = _score(engine, profile, w, sc)
+        base = _score(engine, profile, base_w, sc)
+        reqs = sc.arrival_rps * cp.trace_step_s
+        g_req = act["energy_wh"] / 1000.0 * ci * pue
+        cum += reqs * g_req
+        cum_base += reqs * base["energy_wh"] / 1000.0 * ci * pue
+        acc_sum += act["accuracy"]
+        rep.rows.append(dict(t=t, ci=ci, scheme=scheme, p95_ms=act["p95_ms"], sla_met=bool(act["sla_met"]),
+                             accuracy=act["accuracy"], gco2_per_request=g_req, cumulative_gco2=cum,
+                             optimizing=optimizing))
+    tts = [r.device_ms for r in rep.replans]
+    rep.summary = dict(
+        scheme=scheme, n_gpus=n, ticks=steps, replans=len(rep.replans), total_gco2=cum,
+        carbon_saved_vs_base_pct=100.0 * (cum_base - cum) / cum_base if cum_base > 0 else 0.0,
+        mean_accuracy=acc_sum / steps, base_accuracy=base_sc.obj.base_accuracy,
+        accuracy_delta_vs_base_pct=100.0 * (acc_sum / steps - base_sc.obj.base_accuracy) / base_sc.obj.base_accuracy,
+        sla_violation_ticks=sum(1 for r in rep.rows if not r["sla_met"]),
+        replan_device_ms_mean=float(np.mean(tts)) if tts else 0.0,
+        replan_device_ms_max=float(np.max(tts)) if tts else 0.0,
+        replan_wall_ms_mean=float(np.mean([r.wall_ms for r in rep.replans])) if tts else 0.0,
+        candidates_scored=int(sum(r.evals for r in rep.replans)),
+        reconfigured_gpus=int(sum(r.changed_gpus for r in rep.replans)),
+        downtime_gpu_s=float(sum(r.changed_gpus for r in rep.replans) * cp.reconfig_downtime_s))
+    return rep

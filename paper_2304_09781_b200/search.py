@@ -119,15 +119,18 @@ class ChainsResult:
 
 def exchange_record(engine: CloverEngine, record, group=None):
     """All-gather the 32-byte winner records of all ranks and reduce them in the same
-    fixed order everywhere: one tiny NCCL collective per round."""
+    fixed order everywhere (SPEC:555): one tiny collective per round (NCCL over NVLink;
+    gloo test runs stage the record through host memory)."""
     import torch.distributed as dist
+    from .distributed import gather_records
     if group is None and not (dist.is_available() and dist.is_initialized()):
         return record
-    world = dist.get_world_size(group)
-    if world == 1:
+    if dist.get_world_size(group) == 1:
         return record
-    gathered = record.new_empty(world * 32)
-    dist.all_gather_into_tensor(gathered, record, group=group)
+    if dist.get_backend(group) == "nccl":
+        gathered = gather_records(record, group)
+    else:
+        gathered = gather_records(record.cpu(), group).to(record.device)
     return engine.reduce_records(gathered)
 
 

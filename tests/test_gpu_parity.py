@@ -188,3 +188,24 @@ def test_sweep_two_pods(engine):
     fleets = engine.sweep_decode(pods_e, 2024, best["index"])
     exp = draw_candidate(2024, best["index"], pods_o, DEFAULT_TOPOLOGY)
     assert [(list(f.partitions), list(f.assignments)) for f in fleets] == [(p, a) for p, a in exp]
+
+
+def test_run_trace_matches_oracle_controller(engine, feas64):
+    from oracle.controller import run_trace_clover
+    from paper_2304_09781_b200.controller import run_trace, ControllerParams
+    from paper_2304_09781_b200.profiles import CarbonTrace, synthetic_trace
+    prof = synthetic_profile("efficientnet")
+    T = OracleTables.from_profile(prof)
+    tr = synthetic_trace(hours=1.5)               # 18 ticks
+    ap = AnnealParams(proposal="uniform", max_steps=8)
+    n, chains = 8, 4
+    rep = run_trace(engine, tr, "clover", n, prof, 0.5, ap, ControllerParams(), seed=5, chains=chains)
+    ref = run_trace_clover(tr.samples, n, prof, T, 0.5, ap, 5, chains, feas64)
+    assert len(rep.rows) == len(ref)
+    replan_ticks = [r.tick for r in rep.replans]
+    assert replan_ticks == [x["tick"] for x in ref if x["replanned"]]
+    assert [r.accepted for r in rep.replans] == [x["accepted"] for x in ref if x["replanned"]]
+    for row, x in zip(rep.rows, ref):
+        assert row["sla_met"] == x["sla"]
+        assert row["accuracy"] == x["accuracy"]
+    assert rep.rows[-1]["cumulative_gco2"] == ref[-1]["cum"]
