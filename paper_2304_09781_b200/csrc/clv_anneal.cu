@@ -555,6 +555,9 @@ __global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ 
         __syncthreads();
         done = s.dec_done;
     }
+    // No CTA may leave while a peer can still read its shared memory over DSMEM
+    // (the non-leaders read the leader's decision after the last step).
+    cluster.sync();
 
     if (leader) {
         clv_chain_result r;
