@@ -1,0 +1,21 @@
+#!/bin/bash
+# compute-sanitizer memcheck / racecheck / synccheck on a small chain batch (run on the GPU box)
+PY='import sys; sys.path.insert(0,".")
+import torch
+from paper_2304_09781_b200.engine import CloverEngine
+from paper_2304_09781_b200.profiles import synthetic_profile
+from paper_2304_09781_b200.objective import AnnealParams
+import bench
+eng=CloverEngine(n_max=64); prof=synthetic_profile("efficientnet")
+sc=eng.calibrate(prof,64,350.0,0.5)
+st=bench.make_starts(eng,prof,1,0,3)
+for mode in ("best","uniform"):
+    b=eng.anneal(st,prof,sc,AnnealParams(max_steps=3, proposal=mode),1,cluster=2)
+b=eng.anneal(st,prof,sc,AnnealParams(max_steps=3, proposal="uniform", evaluate="proposal"),1,cluster=3)
+best,_=eng.score_graphs(st,prof,sc)
+eng.oracle_search(prof, eng.calibrate(prof,1,400.0,0.5))
+torch.cuda.synchronize(); print("ok")'
+for tool in memcheck racecheck synccheck; do
+  echo "== $tool"
+  timeout 900 compute-sanitizer --tool $tool --print-limit 10 python -c "$PY" 2>&1 | tail -4
+done
