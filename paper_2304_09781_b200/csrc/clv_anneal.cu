@@ -19,6 +19,7 @@
 // CTA records meet in the leader CTA over DSMEM; the leader applies Eq. 7 and
 // broadcasts the accepted move, which every CTA applies to its own centre.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include "clv_internal.h"
 
 namespace cg = cooperative_groups;
@@ -40,12 +41,12 @@ struct __align__(16) ARow {
 struct __align__(8) RemEnt {            // one removal multiset R (single edge or pair)
     double d0, d1, d2, d3;                 // -(rows of R), exact integers
     unsigned long long mR;                 // presence mask (by latency rank) after removal
-    int base;                              // canonical index of (R, A = {})
-    int off;                               // doubles: first entry of the static move list
     int pre;                               // doubles: exclusive prefix of list lengths
+    int off;                               // doubles: first entry of the static move list
+    unsigned short p;                      // pair index P(r1, r2) (doubles) / edge (singles)
     unsigned short code;                   // slice code of R: sr1*125 + sr2*25 (doubles), sr*5 (singles)
+    unsigned char len;                     // doubles: move-list length
     unsigned char r1, r2;                  // removed edges
-    int len;                               // doubles: move-list length
 };
 
 struct KRec {                              // (key, idx) record; payload hv in uniform mode
@@ -89,7 +90,7 @@ struct __align__(16) AnnealSmem {
     unsigned long long pmask;
     // per-step tables
     RemEnt se[CLV_MAX_EDGES];
-    RemEnt rp[MAXP];
+    RemEnt *rp;                            // -> dynamic tail, E(E+1)/2 entries
     int nPE, nRP, nLen;
     int warp_off[NWARP + 1];
     int warp_len[NWARP + 1];
@@ -218,7 +219,7 @@ __device__ inline void prepare_step(AnnealSmem &s, const FamilyTables &T, int E,
             if (s.w[y] == 1) m &= ~s.rbit[y];
         }
         r.mR = m;
-        r.base = E * E + p * NP;
+        r.p = (unsigned short)p;
         r.off = T.pair_off[p];
         r.len = T.pair_len[p];
         r.pre = lpos;
@@ -236,7 +237,7 @@ __device__ inline void prepare_step(AnnealSmem &s, const FamilyTables &T, int E,
                 RemEnt &r = s.se[c + __popc(bal & ((1u << lane) - 1u))];
                 r.d0 = -s.row[e].thr; r.d1 = -s.row[e].acc; r.d2 = -s.row[e].en; r.d3 = -s.row[e].idle;
                 r.mR = (s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask;
-                r.base = e * E;
+                r.p = (unsigned short)e;
                 r.code = (unsigned short)(s.sl[e] * 5);
                 r.r1 = (unsigned char)e; r.r2 = 0xFF; r.off = 0; r.len = 0; r.pre = 0;
             }
@@ -292,9 +293,22 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, double t, double ac, d
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ AnnealArgs args) {
+__device__ __forceinline__ void fold_score(const Score &sc, long long idx, KRec &rS, KRec &rV, KRec &rP,
+                                           uint64_t seed, uint64_t gchain, uint64_t k) {
+    const unsigned long long key = okey(sc.h);
+    if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; } }
+    else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; } }
+    if (MODE == MODE_UNIFORM_ALL) {
+        const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
+        if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; rP.hv = sc.h; }
+    }
+}
+
+template <int MODE, int MINB, int UNR>
+__global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     AnnealSmem &s = *reinterpret_cast<AnnealSmem *>(smem_raw);
+    if (threadIdx.x == 0) s.rp = reinterpret_cast<RemEnt *>(smem_raw + sizeof(AnnealSmem));
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = (int)cluster.num_blocks();
     const int crank = (int)cluster.block_rank();
@@ -393,7 +407,7 @@ __global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ 
                     ++cnt;
                     const ARow &A = s.row[a];
                     fold<MODE>(s, s.S[0] + R.d0 + A.thr, s.S[1] + R.d1 + A.acc, s.S[2] + R.d2 + A.en,
-                               s.S[3] + R.d3 + A.idle, R.mR | s.rbit[a], (long long)(R.base + a),
+                               s.S[3] + R.d3 + A.idle, R.mR | s.rbit[a], (long long)(R.p * E + a),
                                rS, rV, rP, args.seed, gchain, (uint64_t)k);
                 }
                 i += dI; a += dA;
@@ -404,6 +418,7 @@ __global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ 
         {
             const int lane = tid & 31, wid = tid >> 5;
             const int ND = s.nLen;
+            const int NPc = E * (E + 1) / 2;
             const int W = CL * NWARP;
             const int chunk = (((ND + W - 1) / W) + 31) & ~31;
             const int gw = crank * NWARP + wid;
@@ -418,18 +433,49 @@ __global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ 
                 }
                 int j = lo;
                 const uint32_t *plist = T.pair_list;
-                for (; t < tend; t += 32) {
-                    while (t >= s.rp[j].pre + s.rp[j].len) ++j;
-                    const RemEnt &R = s.rp[j];
-                    const uint32_t ent = __ldg(plist + R.off + (t - R.pre));
-                    if (s.feasD[R.code + ((ent >> 12) & 31)]) {
-                        ++cnt;
-                        const int a1 = ent & 63, a2 = (ent >> 6) & 63;
-                        const ARow &A1 = s.row[a1], &A2 = s.row[a2];
-                        fold<MODE>(s, s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
-                                   s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
-                                   R.mR | s.rbit[a1] | s.rbit[a2], (long long)(R.base + (int)(ent >> 17)),
-                                   rS, rV, rP, args.seed, gchain, (uint64_t)k);
+                if (UNR == 1) {
+                    for (; t < tend; t += 32) {
+                        while (t >= s.rp[j].pre + s.rp[j].len) ++j;
+                        const RemEnt &R = s.rp[j];
+                        const uint32_t ent = __ldg(plist + R.off + (t - R.pre));
+                        if (s.feasD[R.code + ((ent >> 12) & 31)]) {
+                            ++cnt;
+                            const int a1 = ent & 63, a2 = (ent >> 6) & 63;
+                            const ARow &A1 = s.row[a1], &A2 = s.row[a2];
+                            fold<MODE>(s, s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
+                                       s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
+                                       R.mR | s.rbit[a1] | s.rbit[a2], (long long)E * E + (long long)R.p * NPc + (int)(ent >> 17),
+                                       rS, rV, rP, args.seed, gchain, (uint64_t)k);
+                        }
+                    }
+                } else {
+                    // two independent candidates per iteration (ILP across the fp64 chains)
+                    for (; t < tend; t += 64) {
+                        while (t >= s.rp[j].pre + s.rp[j].len) ++j;
+                        const int t2 = t + 32;
+                        const bool has2 = t2 < tend;
+                        int j2 = j;
+                        if (has2) while (t2 >= s.rp[j2].pre + s.rp[j2].len) ++j2;
+                        const RemEnt &R = s.rp[j];
+                        const RemEnt &Q = s.rp[j2];
+                        const uint32_t e1 = __ldg(plist + R.off + (t - R.pre));
+                        const uint32_t e2 = has2 ? __ldg(plist + Q.off + (t2 - Q.pre)) : 0u;
+                        const bool ok1 = s.feasD[R.code + ((e1 >> 12) & 31)];
+                        const bool ok2 = has2 && s.feasD[Q.code + ((e2 >> 12) & 31)];
+                        const int a1 = e1 & 63, a2 = (e1 >> 6) & 63, b1 = e2 & 63, b2 = (e2 >> 6) & 63;
+                        const ARow &A1 = s.row[a1], &A2 = s.row[a2], &B1 = s.row[b1], &B2 = s.row[b2];
+                        const double lm1 = lmax_of(s, R.mR | s.rbit[a1] | s.rbit[a2]);
+                        const double lm2 = lmax_of(s, Q.mR | s.rbit[b1] | s.rbit[b2]);
+                        const Score sc1 = epilogue_d(s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
+                                                     s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
+                                                     lm1, s.ec);
+                        const Score sc2 = epilogue_d(s.S[0] + Q.d0 + B1.thr + B2.thr, s.S[1] + Q.d1 + B1.acc + B2.acc,
+                                                     s.S[2] + Q.d2 + B1.en + B2.en, s.S[3] + Q.d3 + B1.idle + B2.idle,
+                                                     lm2, s.ec);
+                        cnt += (unsigned long long)ok1 + (unsigned long long)ok2;
+                        if (ok1) fold_score<MODE>(sc1, (long long)E * E + (long long)R.p * NPc + (int)(e1 >> 17), rS, rV, rP, args.seed, gchain, (uint64_t)k);
+                        if (ok2) fold_score<MODE>(sc2, (long long)E * E + (long long)Q.p * NPc + (int)(e2 >> 17), rS, rV, rP, args.seed, gchain, (uint64_t)k);
+                        j = j2;
                     }
                 }
             }
@@ -581,12 +627,13 @@ __global__ void __launch_bounds__(ANT, 3) anneal_kernel(const __grid_constant__ 
     }
 }
 
-template <int MODE>
+template <int MODE, int MINB, int UNR>
 static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
-    const size_t smem = sizeof(AnnealSmem);
-    cudaError_t e = cudaFuncSetAttribute(anneal_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = anneal_kernel<MODE, MINB, UNR>;
+    const size_t smem = sizeof(AnnealSmem) + sizeof(RemEnt) * (size_t)(a.E * (a.E + 1) / 2);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(anneal_kernel<MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(ANT, 1, 1);
@@ -605,8 +652,7 @@ static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream
             cfg.gridDim = dim3((unsigned)(a.n_chains * c), 1, 1);
             attr[0].val.clusterDim.x = (unsigned)c;
             int clusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&clusters, anneal_kernel<MODE>, &cfg) == cudaSuccess &&
-                clusters >= a.n_chains) {
+            if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) == cudaSuccess && clusters >= a.n_chains) {
                 cluster_size = c;
                 break;
             }
@@ -615,13 +661,26 @@ static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream
     }
     cfg.gridDim = dim3((unsigned)(a.n_chains * cluster_size), 1, 1);
     attr[0].val.clusterDim.x = (unsigned)cluster_size;
-    return cudaLaunchKernelEx(&cfg, anneal_kernel<MODE>, a);
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+static int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
 }
 
 cudaError_t launch_anneal(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
-    if (a.proposal == 0) return launch_mode<MODE_BEST_ALL>(a, cluster_size, st);
-    if (a.evaluate == 0) return launch_mode<MODE_UNIFORM_ALL>(a, cluster_size, st);
-    return launch_mode<MODE_UNIFORM_PROPOSAL>(a, cluster_size, st);
+    if (a.proposal == 0) {
+        // tuning variants of the headline mode (CLV_ANNEAL_VARIANT, default 0)
+        switch (env_int("CLV_ANNEAL_VARIANT", 0)) {
+            case 1: return launch_mode<MODE_BEST_ALL, 3, 2>(a, cluster_size, st);
+            case 2: return launch_mode<MODE_BEST_ALL, 4, 1>(a, cluster_size, st);
+            case 3: return launch_mode<MODE_BEST_ALL, 2, 2>(a, cluster_size, st);
+            default: return launch_mode<MODE_BEST_ALL, 3, 1>(a, cluster_size, st);
+        }
+    }
+    if (a.evaluate == 0) return launch_mode<MODE_UNIFORM_ALL, 3, 1>(a, cluster_size, st);
+    return launch_mode<MODE_UNIFORM_PROPOSAL, 3, 1>(a, cluster_size, st);
 }
 
 }  // namespace clv

@@ -582,7 +582,7 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
     a.fam = ctx->fam_dev + family; a.F = feas_view(ctx); a.ec = ctx->ec_dev; a.n_ec = n_params;
     a.t_init = ap->t_init; a.cooling = ap->cooling_step; a.t_floor = ap->t_floor;
     a.stall_limit = ap->stall_limit; a.max_steps = ap->max_steps; a.proposal = ap->proposal; a.evaluate = ap->evaluate;
-    a.n = n; a.n_chains = n_chains; a.chain_base = chain_base; a.seed = seed;
+    a.n = n; a.n_chains = n_chains; a.E = ctx->fam[family].E; a.chain_base = chain_base; a.seed = seed;
     a.start_w = start_w_dev; a.res = results_dev; a.best_w = best_w_dev; a.final_w = final_w_dev; a.log = log_dev;
     CLV_CUDA(launch_anneal(a, cluster_size, st), "anneal");
     return CLV_OK;

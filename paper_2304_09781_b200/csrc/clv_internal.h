@@ -130,7 +130,7 @@ struct AnnealArgs {
     int n_ec;
     double t_init, cooling, t_floor;
     int stall_limit, max_steps, proposal, evaluate;
-    int n, n_chains;
+    int n, n_chains, E;
     long long chain_base;
     uint64_t seed;
     const uint16_t *start_w;
