@@ -90,7 +90,6 @@ struct __align__(16) AnnealSmem {
     unsigned long long pmask;
     // per-step tables
     RemEnt se[CLV_MAX_EDGES];
-    RemEnt *rp;                            // -> dynamic tail, E(E+1)/2 entries
     int nPE, nRP, nLen;
     int warp_off[NWARP + 1];
     int warp_len[NWARP + 1];
@@ -170,7 +169,8 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
 // present edges -- every CTA of the cluster must build identical tables because
 // the cluster partitions the move space by table position -- plus the
 // feasibility bytes of all 25 single / 625 double slice deltas.
-__device__ inline void prepare_step(AnnealSmem &s, const FamilyTables &T, int E, int n, const FeasView &F) {
+__device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, const FamilyTables &T, int E, int n,
+                                             const FeasView &F) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int NP = E * (E + 1) / 2;
     const int PER = (NP + ANT - 1) / ANT;          // consecutive pairs per thread (<= 4)
@@ -207,7 +207,7 @@ __device__ inline void prepare_step(AnnealSmem &s, const FamilyTables &T, int E,
         const int x = s.pair_tab[p] & 0xFF, y = s.pair_tab[p] >> 8;
         const bool ok = (x == y) ? (s.w[x] >= 2) : (s.w[x] > 0 && s.w[y] > 0);
         if (!ok) continue;
-        RemEnt &r = s.rp[pos++];
+        RemEnt &r = rp[pos++];
         r.d0 = -(s.row[x].thr + s.row[y].thr);
         r.d1 = -(s.row[x].acc + s.row[y].acc);
         r.d2 = -(s.row[x].en + s.row[y].en);
@@ -308,7 +308,7 @@ template <int MODE, int MINB, int UNR>
 __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     AnnealSmem &s = *reinterpret_cast<AnnealSmem *>(smem_raw);
-    if (threadIdx.x == 0) s.rp = reinterpret_cast<RemEnt *>(smem_raw + sizeof(AnnealSmem));
+    RemEnt *const rp = reinterpret_cast<RemEnt *>(smem_raw + sizeof(AnnealSmem));   // dynamic tail, E(E+1)/2
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = (int)cluster.num_blocks();
     const int crank = (int)cluster.block_rank();
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     const unsigned long long mem_ok = s.mem_ok;
 
     for (int k = 0; !done; ++k) {
-        prepare_step(s, T, E, n, args.F);
+        prepare_step(s, rp, T, E, n, args.F);
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
         unsigned long long cnt = 0;
         // ---- singles: (present edge i, target edge a)
@@ -429,14 +429,14 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 const int t0 = t < ND ? t : ND - 1;
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
-                    if (s.rp[mid].pre <= t0) lo = mid; else hi = mid - 1;
+                    if (rp[mid].pre <= t0) lo = mid; else hi = mid - 1;
                 }
                 int j = lo;
                 const uint32_t *plist = T.pair_list;
                 if (UNR == 1) {
                     for (; t < tend; t += 32) {
-                        while (t >= s.rp[j].pre + s.rp[j].len) ++j;
-                        const RemEnt &R = s.rp[j];
+                        while (t >= rp[j].pre + rp[j].len) ++j;
+                        const RemEnt &R = rp[j];
                         const uint32_t ent = __ldg(plist + R.off + (t - R.pre));
                         if (s.feasD[R.code + ((ent >> 12) & 31)]) {
                             ++cnt;
@@ -451,13 +451,13 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 } else {
                     // two independent candidates per iteration (ILP across the fp64 chains)
                     for (; t < tend; t += 64) {
-                        while (t >= s.rp[j].pre + s.rp[j].len) ++j;
+                        while (t >= rp[j].pre + rp[j].len) ++j;
                         const int t2 = t + 32;
                         const bool has2 = t2 < tend;
                         int j2 = j;
-                        if (has2) while (t2 >= s.rp[j2].pre + s.rp[j2].len) ++j2;
-                        const RemEnt &R = s.rp[j];
-                        const RemEnt &Q = s.rp[j2];
+                        if (has2) while (t2 >= rp[j2].pre + rp[j2].len) ++j2;
+                        const RemEnt &R = rp[j];
+                        const RemEnt &Q = rp[j2];
                         const uint32_t e1 = __ldg(plist + R.off + (t - R.pre));
                         const uint32_t e2 = has2 ? __ldg(plist + Q.off + (t2 - Q.pre)) : 0u;
                         const bool ok1 = s.feasD[R.code + ((e1 >> 12) & 31)];
