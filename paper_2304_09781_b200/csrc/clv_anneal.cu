@@ -40,6 +40,7 @@ struct __align__(16) ARow {
 
 struct __align__(8) RemEnt {            // one removal multiset R (single edge or pair)
     double d0, d1, d2, d3;                 // -(rows of R), exact integers
+    float f0, f1, f2, f3;                  // the same deltas in fp32 (screening only)
     unsigned long long mR;                 // presence mask (by latency rank) after removal
     int pre;                               // doubles: exclusive prefix of list lengths
     int off;                               // doubles: first entry of the static move list
@@ -49,25 +50,26 @@ struct __align__(8) RemEnt {            // one removal multiset R (single edge o
     unsigned char r1, r2;                  // removed edges
 };
 
-struct KRec {                              // (key, idx) record; payload hv in uniform mode
+struct KRec {                              // (key, idx) record; payload hv (uniform proposals)
     unsigned long long key;
-    long long idx;
+    int idx;                               // canonical indices are < 2^31
     double hv;
 };
 
-__device__ __forceinline__ bool krec_less(unsigned long long ka, long long ia, const KRec &b) {
+__device__ __forceinline__ bool krec_less(unsigned long long ka, int ia, const KRec &b) {
     return ka < b.key || (ka == b.key && ia < b.idx);
 }
 __device__ __forceinline__ KRec krec_none() {
-    KRec r; r.key = ~0ULL; r.idx = 0x7FFFFFFFFFFFFFFFLL; r.hv = 0.0; return r;
+    KRec r; r.key = ~0ULL; r.idx = 0x7FFFFFFF; r.hv = 0.0; return r;
 }
+template <bool PAYLOAD>
 __device__ __forceinline__ KRec krec_min_warp(KRec r) {
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) {
         KRec o;
         o.key = __shfl_xor_sync(0xFFFFFFFFu, r.key, m);
         o.idx = __shfl_xor_sync(0xFFFFFFFFu, r.idx, m);
-        o.hv = __shfl_xor_sync(0xFFFFFFFFu, r.hv, m);
+        o.hv = PAYLOAD ? __shfl_xor_sync(0xFFFFFFFFu, r.hv, m) : 0.0;
         if (krec_less(o.key, o.idx, r)) r = o;
     }
     return r;
@@ -75,7 +77,11 @@ __device__ __forceinline__ KRec krec_min_warp(KRec r) {
 
 struct __align__(16) AnnealSmem {
     ARow row[CLV_MAX_EDGES];
+    float4 rowf[CLV_MAX_EDGES];            // fp32 copies of the rows (screening only)
     double lat_by_rank[CLV_MAX_EDGES];
+    float latf_by_rank[CLV_MAX_EDGES];
+    float Sf[4];                           // fp32 copy of the centre sums
+    float ecf[12];                         // fp32 epilogue constants (screening only)
     unsigned long long rbit[CLV_MAX_EDGES];
     unsigned long long adjm[CLV_MAX_EDGES];
     EvalConst ec;
@@ -83,6 +89,8 @@ struct __align__(16) AnnealSmem {
     short Pt[CLV_MAX_EDGES + 1];           // P(x, y) = Pt[x] + y
     unsigned char sl[CLV_MAX_EDGES];
     unsigned short pair_tab[MAXP];
+    int pair_off[MAXP];                    // static move lists (staged from FamilyTables)
+    unsigned char pair_len[MAXP];
     // centre
     int w[CLV_MAX_EDGES];
     double S[4];
@@ -112,14 +120,15 @@ __device__ __forceinline__ double lmax_of(const AnnealSmem &s, unsigned long lon
 }
 
 // canonical index -> move (r1, r2, a1, a2; 0xFF = absent)
-__device__ inline void decode_move(const AnnealSmem &s, int E, long long idx, int &r1, int &r2, int &a1, int &a2) {
-    if (idx < (long long)E * E) {
-        r1 = (int)(idx / E); a1 = (int)(idx % E); r2 = 0xFF; a2 = 0xFF;
+__device__ inline void decode_move(const AnnealSmem &s, int E, long long idx64, int &r1, int &r2, int &a1, int &a2) {
+    const unsigned idx = (unsigned)idx64;          // canonical indices are < 2^31
+    if (idx < (unsigned)(E * E)) {
+        r1 = (int)(idx / (unsigned)E); a1 = (int)(idx - (unsigned)r1 * E); r2 = 0xFF; a2 = 0xFF;
         return;
     }
-    const int NP = E * (E + 1) / 2;
-    const long long u = idx - (long long)E * E;
-    const int p = (int)(u / NP), q = (int)(u - (long long)p * NP);
+    const unsigned NP = (unsigned)(E * (E + 1) / 2);
+    const unsigned u = idx - (unsigned)(E * E);
+    const int p = (int)(u / NP), q = (int)(u - (unsigned)p * NP);
     r1 = s.pair_tab[p] & 0xFF; r2 = s.pair_tab[p] >> 8;
     a1 = s.pair_tab[q] & 0xFF; a2 = s.pair_tab[q] >> 8;
 }
@@ -174,12 +183,37 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, const Fa
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int NP = E * (E + 1) / 2;
     const int PER = (NP + ANT - 1) / ANT;          // consecutive pairs per thread (<= 4)
+    bool refresh = false;
+#pragma unroll
+    for (int k = 0; k < CLV_K; ++k) refresh |= (s.svec[k] != s.fsvec[k]);
+    if (threadIdx.x < 4) s.Sf[threadIdx.x] = (float)s.S[threadIdx.x];
+    bool fres[3] = {false, false, false};
+    if (refresh) {                                 // uniform across the CTA
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const int t = threadIdx.x + q * ANT;
+            if (t >= 650) continue;
+            int v[CLV_K];
+#pragma unroll
+            for (int k = 0; k < CLV_K; ++k) v[k] = s.svec[k];
+            bool ok;
+            if (t < 25) {
+                v[t / 5] -= 1; v[t % 5] += 1;
+                ok = v[t / 5] >= 0;
+            } else {
+                const int u = t - 25;
+                v[u / 125] -= 1; v[(u / 25) % 5] -= 1; v[(u / 5) % 5] += 1; v[u % 5] += 1;
+                ok = v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[3] >= 0 && v[4] >= 0;
+            }
+            fres[q] = ok && feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
+        }
+    }
     const int p0 = threadIdx.x * PER;
     int cnt = 0, lsum = 0;
     for (int p = p0; p < p0 + PER && p < NP; ++p) {
         const int x = s.pair_tab[p] & 0xFF, y = s.pair_tab[p] >> 8;
         const bool ok = (x == y) ? (s.w[x] >= 2) : (s.w[x] > 0 && s.w[y] > 0);
-        if (ok) { ++cnt; lsum += T.pair_len[p]; }
+        if (ok) { ++cnt; lsum += s.pair_len[p]; }
     }
     // block exclusive scan of (cnt, lsum) in thread order
     int ic = cnt, il = lsum;
@@ -212,6 +246,8 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, const Fa
         r.d1 = -(s.row[x].acc + s.row[y].acc);
         r.d2 = -(s.row[x].en + s.row[y].en);
         r.d3 = -(s.row[x].idle + s.row[y].idle);
+        r.f0 = -(s.rowf[x].x + s.rowf[y].x); r.f1 = -(s.rowf[x].y + s.rowf[y].y);
+        r.f2 = -(s.rowf[x].z + s.rowf[y].z); r.f3 = -(s.rowf[x].w + s.rowf[y].w);
         unsigned long long m = s.pmask;
         if (x == y) { if (s.w[x] == 2) m &= ~s.rbit[x]; }
         else {
@@ -220,8 +256,8 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, const Fa
         }
         r.mR = m;
         r.p = (unsigned short)p;
-        r.off = T.pair_off[p];
-        r.len = T.pair_len[p];
+        r.off = s.pair_off[p];
+        r.len = s.pair_len[p];
         r.pre = lpos;
         lpos += r.len;
         r.code = (unsigned short)(s.sl[x] * 125 + s.sl[y] * 25);
@@ -236,6 +272,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, const Fa
             if (ok) {
                 RemEnt &r = s.se[c + __popc(bal & ((1u << lane) - 1u))];
                 r.d0 = -s.row[e].thr; r.d1 = -s.row[e].acc; r.d2 = -s.row[e].en; r.d3 = -s.row[e].idle;
+                r.f0 = -s.rowf[e].x; r.f1 = -s.rowf[e].y; r.f2 = -s.rowf[e].z; r.f3 = -s.rowf[e].w;
                 r.mR = (s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask;
                 r.p = (unsigned short)e;
                 r.code = (unsigned short)(s.sl[e] * 5);
@@ -246,66 +283,111 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, const Fa
         if (lane == 0) s.nPE = c;
     }
     // slice-delta feasibility: only when the centre's slice multiset changed
-    // (variant swaps keep it), the cache stays valid
-    bool same = true;
-#pragma unroll
-    for (int k = 0; k < CLV_K; ++k) same &= (s.svec[k] == s.fsvec[k]);
-    __syncthreads();
-    if (!same) {
-        for (int t = threadIdx.x; t < 650; t += ANT) {
-            int v[CLV_K];
-#pragma unroll
-            for (int k = 0; k < CLV_K; ++k) v[k] = s.svec[k];
-            if (t < 25) {
-                v[t / 5] -= 1; v[t % 5] += 1;
-                s.feasS[t] = v[t / 5] >= 0 && feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
-            } else {
-                const int u = t - 25;
-                v[u / 125] -= 1; v[(u / 25) % 5] -= 1; v[(u / 5) % 5] += 1; v[u % 5] += 1;
-                s.feasD[u] = v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[3] >= 0 && v[4] >= 0 &&
-                             feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
-            }
+    // (variant swaps keep it).  The loads were issued at the top of prepare_step.
+    if (refresh) {
+        for (int q = 0; q < 3; ++q) {
+            const int t = threadIdx.x + q * ANT;
+            if (t < 25) s.feasS[t] = fres[q];
+            else if (t < 650) s.feasD[t - 25] = fres[q];
         }
-        __syncthreads();
         if (threadIdx.x < CLV_K) s.fsvec[threadIdx.x] = s.svec[threadIdx.x];
-        __syncthreads();
     }
+    __syncthreads();
 }
 
-// Fold one valid neighbour into the thread's records.
-template <int MODE>
-__device__ __forceinline__ void fold(const AnnealSmem &s, double t, double ac, double en, double id,
-                                     unsigned long long m, long long idx, KRec &rS, KRec &rV, KRec &rP,
-                                     uint64_t seed, uint64_t gchain, uint64_t k) {
-    if (MODE != MODE_UNIFORM_PROPOSAL) {
-        const Score sc = epilogue_d(t, ac, en, id, lmax_of(s, m), s.ec);
-        const unsigned long long key = okey(sc.h);
-        if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; } }
-        else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; } }
-        if (MODE == MODE_UNIFORM_ALL) {
-            const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
-            if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; rP.hv = sc.h; }
-        }
-    } else {
+// fp32 screening bound: a candidate is scored exactly
+// only if its fp32 estimate, widened by a generous error bound, could beat the
+// thread's current record of its SLA class (or, for uniform proposals, if its hash
+// would become the proposal).  Records are exact minima of the exactly scored
+// candidates, and a skipped candidate is provably worse than a scored one, so the
+// selection is bit-identical to scoring everything.
+enum { EC_RQ = 0, EC_ENS, EC_IDLES, EC_I3600R, EC_RSAT, EC_AB, EC_KA, EC_KC, EC_LAM, EC_SLO, EC_STRICT };
+
+__device__ __forceinline__ bool screen_out(const AnnealSmem &s, float t, float ac, float en, float id, float lmax,
+                                           const KRec &rS, const KRec &rV) {
+    const float *c = s.ecf;
+    const float inv = __frcp_rn(t);
+    const float A = ac * inv;
+    const float rho = c[EC_RQ] * inv;
+    const float e = (en * inv) * c[EC_ENS];
+    const float rc = fminf(rho, 1.0f);
+    const float E = e + ((1.0f - rc) * (id * c[EC_IDLES])) * c[EC_I3600R];
+    const float rq = fminf(rho, c[EC_RSAT]);
+    const float den = 1.0f - rq;
+    const float L = lmax * __frcp_rn(den);
+    const float EkC = E * c[EC_KC];
+    const float dA = (A - c[EC_AB]) * c[EC_KA];
+    const float f = c[EC_LAM] * (100.0f - EkC) + (1.0f - c[EC_LAM]) * dA;
+    // absolute error bound of f (~8x the worst-case fp32 propagation) and relative bound of L
+    const float M = 4e-6f * (100.0f + fabsf(EkC) + (A + c[EC_AB]) * c[EC_KA]);
+    const float relL = 4e-6f * (2.0f + __frcp_rn(den));
+    const float slo = c[EC_SLO];
+    if (L * (1.0f + relL) < slo) {                       // SLA surely met: h = -f
+        return rS.key != ~0ULL && (double)(-f - M) > rS.hv;
+    }
+    if (L * (1.0f - relL) > slo && fabsf(f) > M) {       // SLA surely violated, sign of f sure
+        const bool soft = f >= 0.0f || c[EC_STRICT] != 0.0f;
+        const float q = soft ? slo * __frcp_rn(L) : L * __frcp_rn(slo);
+        const float h = -f * q;
+        const float err = 1.01f * q * (M + fabsf(f) * 2.0f * relL) + 1e-6f * fabsf(h);
+        return rV.key != ~0ULL && (double)(h - err) > rV.hv;
+    }
+    return false;
+}
+
+template <int MODE, bool PAIR>
+__device__ __forceinline__ void consider(const AnnealSmem &s, const RemEnt &R, int a1, int a2, int idx,
+                                         KRec &rS, KRec &rV, KRec &rP, uint64_t seed, uint64_t gchain,
+                                         uint64_t k) {
+    if (MODE == MODE_UNIFORM_PROPOSAL) {
         const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
         if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; }
+        return;
     }
-}
-
-template <int MODE>
-__device__ __forceinline__ void fold_score(const Score &sc, long long idx, KRec &rS, KRec &rV, KRec &rP,
-                                           uint64_t seed, uint64_t gchain, uint64_t k) {
-    const unsigned long long key = okey(sc.h);
-    if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; } }
-    else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; } }
+    unsigned long long hk = 0;
+    bool wantP = false;
     if (MODE == MODE_UNIFORM_ALL) {
-        const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
-        if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; rP.hv = sc.h; }
+        hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
+        wantP = krec_less(hk, idx, rP);
     }
+    const unsigned long long m = PAIR ? (R.mR | s.rbit[a1] | s.rbit[a2]) : (R.mR | s.rbit[a1]);
+    const int top = 63 - __clzll((long long)m);
+    if (!wantP) {
+        const float4 x = s.rowf[a1];
+        float t = s.Sf[0] + R.f0 + x.x, ac = s.Sf[1] + R.f1 + x.y, en = s.Sf[2] + R.f2 + x.z, id = s.Sf[3] + R.f3 + x.w;
+        if (PAIR) {
+            const float4 y = s.rowf[a2];
+            t += y.x; ac += y.y; en += y.z; id += y.w;
+        }
+        if (screen_out(s, t, ac, en, id, s.latf_by_rank[top], rS, rV)) return;
+    }
+    const ARow &A1 = s.row[a1];
+    double t = s.S[0] + R.d0 + A1.thr, ac = s.S[1] + R.d1 + A1.acc, en = s.S[2] + R.d2 + A1.en,
+           id = s.S[3] + R.d3 + A1.idle;
+    if (PAIR) {
+        const ARow &A2 = s.row[a2];
+        t += A2.thr; ac += A2.acc; en += A2.en; id += A2.idle;
+    }
+    const Score sc = epilogue_d(t, ac, en, id, s.lat_by_rank[top], s.ec);
+    const unsigned long long key = okey(sc.h);
+    if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; rS.hv = sc.h; } }
+    else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; rV.hv = sc.h; } }
+    if (MODE == MODE_UNIFORM_ALL && wantP) { rP.key = hk; rP.idx = idx; rP.hv = sc.h; }
 }
 
-template <int MODE, int MINB, int UNR>
+// Optional phase profiler (CLV_ANNEAL_VARIANT=9): thread 0 of each CTA accumulates
+// clock64 deltas between consecutive marks into args.prof[(chain*CL+rank)*8 + phase].
+#define PROF_MARK(ph)                                                                  \
+    if (PROF && threadIdx.x == 0) {                                                    \
+        const long long _now = clock64();                                              \
+        if ((ph) > 0) prof_acc[(ph) - 1] += _now - prof_last;                          \
+        prof_last = _now;                                                              \
+    }
+
+template <int MODE, int MINB, int UNR, bool PROF = false>
 __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
+    long long prof_acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    long long prof_last = 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     AnnealSmem &s = *reinterpret_cast<AnnealSmem *>(smem_raw);
     RemEnt *const rp = reinterpret_cast<RemEnt *>(smem_raw + sizeof(AnnealSmem));   // dynamic tail, E(E+1)/2
@@ -327,6 +409,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         s.row[e].en = (double)T.en_q[e];
         s.row[e].idle = (double)T.idle_q[e % 5];
         s.lat_by_rank[e] = T.lat_by_rank[e];
+        s.latf_by_rank[e] = (float)T.lat_by_rank[e];
+        s.rowf[e] = make_float4((float)T.thr_q[e], (float)T.acc_q[e], (float)T.en_q[e], (float)T.idle_q[e % 5]);
         s.rbit[e] = 1ULL << T.rank[e];
         s.sl[e] = (unsigned char)(e % 5);
         unsigned long long am = 0;
@@ -337,9 +421,15 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     for (int x = tid; x <= E; x += ANT) s.Pt[x] = (short)(x * E - (x * (x - 1)) / 2 - x);
     for (int x = tid; x < E; x += ANT)
         for (int y = x; y < E; ++y) s.pair_tab[x * E - (x * (x - 1)) / 2 + (y - x)] = (unsigned short)(x | (y << 8));
+    for (int p = tid; p < E * (E + 1) / 2; p += ANT) { s.pair_off[p] = T.pair_off[p]; s.pair_len[p] = T.pair_len[p]; }
     if (tid == 0) {
         s.mem_ok = T.mem_ok;
         s.ec = args.ec[args.n_ec == 1 ? 0 : chain];
+        const EvalConst &c = s.ec;
+        s.ecf[EC_RQ] = (float)c.R_q; s.ecf[EC_ENS] = (float)c.en_scale; s.ecf[EC_IDLES] = (float)c.idle_scale;
+        s.ecf[EC_I3600R] = (float)c.inv_3600R; s.ecf[EC_RSAT] = (float)c.rho_sat; s.ecf[EC_AB] = (float)c.a_base;
+        s.ecf[EC_KA] = (float)c.kA; s.ecf[EC_KC] = (float)c.kC; s.ecf[EC_LAM] = (float)c.lam;
+        s.ecf[EC_SLO] = (float)c.slo; s.ecf[EC_STRICT] = (float)c.strict;
     }
     __syncthreads();
     if (tid == 0) {
@@ -392,7 +482,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     const unsigned long long mem_ok = s.mem_ok;
 
     for (int k = 0; !done; ++k) {
+        PROF_MARK(0);
         prepare_step(s, rp, T, E, n, args.F);
+        PROF_MARK(1);
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
         unsigned long long cnt = 0;
         // ---- singles: (present edge i, target edge a)
@@ -405,10 +497,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 const bool ok = (a != R.r1) && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]];
                 if (ok) {
                     ++cnt;
-                    const ARow &A = s.row[a];
-                    fold<MODE>(s, s.S[0] + R.d0 + A.thr, s.S[1] + R.d1 + A.acc, s.S[2] + R.d2 + A.en,
-                               s.S[3] + R.d3 + A.idle, R.mR | s.rbit[a], (long long)(R.p * E + a),
-                               rS, rV, rP, args.seed, gchain, (uint64_t)k);
+                    consider<MODE, false>(s, R, a, 0, (int)(R.p * E + a), rS, rV, rP, args.seed, gchain, (uint64_t)k);
                 }
                 i += dI; a += dA;
                 if (a >= E) { a -= E; ++i; }
@@ -433,49 +522,14 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 }
                 int j = lo;
                 const uint32_t *plist = T.pair_list;
-                if (UNR == 1) {
-                    for (; t < tend; t += 32) {
-                        while (t >= rp[j].pre + rp[j].len) ++j;
-                        const RemEnt &R = rp[j];
-                        const uint32_t ent = __ldg(plist + R.off + (t - R.pre));
-                        if (s.feasD[R.code + ((ent >> 12) & 31)]) {
-                            ++cnt;
-                            const int a1 = ent & 63, a2 = (ent >> 6) & 63;
-                            const ARow &A1 = s.row[a1], &A2 = s.row[a2];
-                            fold<MODE>(s, s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
-                                       s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
-                                       R.mR | s.rbit[a1] | s.rbit[a2], (long long)E * E + (long long)R.p * NPc + (int)(ent >> 17),
-                                       rS, rV, rP, args.seed, gchain, (uint64_t)k);
-                        }
-                    }
-                } else {
-                    // two independent candidates per iteration (ILP across the fp64 chains)
-                    for (; t < tend; t += 64) {
-                        while (t >= rp[j].pre + rp[j].len) ++j;
-                        const int t2 = t + 32;
-                        const bool has2 = t2 < tend;
-                        int j2 = j;
-                        if (has2) while (t2 >= rp[j2].pre + rp[j2].len) ++j2;
-                        const RemEnt &R = rp[j];
-                        const RemEnt &Q = rp[j2];
-                        const uint32_t e1 = __ldg(plist + R.off + (t - R.pre));
-                        const uint32_t e2 = has2 ? __ldg(plist + Q.off + (t2 - Q.pre)) : 0u;
-                        const bool ok1 = s.feasD[R.code + ((e1 >> 12) & 31)];
-                        const bool ok2 = has2 && s.feasD[Q.code + ((e2 >> 12) & 31)];
-                        const int a1 = e1 & 63, a2 = (e1 >> 6) & 63, b1 = e2 & 63, b2 = (e2 >> 6) & 63;
-                        const ARow &A1 = s.row[a1], &A2 = s.row[a2], &B1 = s.row[b1], &B2 = s.row[b2];
-                        const double lm1 = lmax_of(s, R.mR | s.rbit[a1] | s.rbit[a2]);
-                        const double lm2 = lmax_of(s, Q.mR | s.rbit[b1] | s.rbit[b2]);
-                        const Score sc1 = epilogue_d(s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
-                                                     s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
-                                                     lm1, s.ec);
-                        const Score sc2 = epilogue_d(s.S[0] + Q.d0 + B1.thr + B2.thr, s.S[1] + Q.d1 + B1.acc + B2.acc,
-                                                     s.S[2] + Q.d2 + B1.en + B2.en, s.S[3] + Q.d3 + B1.idle + B2.idle,
-                                                     lm2, s.ec);
-                        cnt += (unsigned long long)ok1 + (unsigned long long)ok2;
-                        if (ok1) fold_score<MODE>(sc1, (long long)E * E + (long long)R.p * NPc + (int)(e1 >> 17), rS, rV, rP, args.seed, gchain, (uint64_t)k);
-                        if (ok2) fold_score<MODE>(sc2, (long long)E * E + (long long)Q.p * NPc + (int)(e2 >> 17), rS, rV, rP, args.seed, gchain, (uint64_t)k);
-                        j = j2;
+                for (; t < tend; t += 32) {
+                    while (t >= rp[j].pre + rp[j].len) ++j;
+                    const RemEnt &R = rp[j];
+                    const uint32_t ent = __ldg(plist + R.off + (t - R.pre));
+                    if (s.feasD[R.code + ((ent >> 12) & 31)]) {
+                        ++cnt;
+                        consider<MODE, true>(s, R, ent & 63, (ent >> 6) & 63, E * E + (int)R.p * NPc + (int)(ent >> 17),
+                                             rS, rV, rP, args.seed, gchain, (uint64_t)k);
                     }
                 }
             }
@@ -483,8 +537,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         // ---- CTA reduction, then DSMEM publish into the leader's slots
         {
             const int lane = tid & 31, wid = tid >> 5;
-            if (MODE != MODE_UNIFORM_PROPOSAL) { rS = krec_min_warp(rS); rV = krec_min_warp(rV); }
-            if (MODE != MODE_BEST_ALL) rP = krec_min_warp(rP);
+            if (MODE != MODE_UNIFORM_PROPOSAL) { rS = krec_min_warp<false>(rS); rV = krec_min_warp<false>(rV); }
+            if (MODE != MODE_BEST_ALL) rP = krec_min_warp<MODE == MODE_UNIFORM_ALL>(rP);
 #pragma unroll
             for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, m);
             if (lane == 0) { s.wS[wid] = rS; s.wV[wid] = rV; s.wP[wid] = rP; s.wc[wid] = cnt; }
@@ -494,8 +548,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 rV = lane < NWARP ? s.wV[lane] : krec_none();
                 rP = lane < NWARP ? s.wP[lane] : krec_none();
                 cnt = lane < NWARP ? s.wc[lane] : 0ULL;
-                if (MODE != MODE_UNIFORM_PROPOSAL) { rS = krec_min_warp(rS); rV = krec_min_warp(rV); }
-                if (MODE != MODE_BEST_ALL) rP = krec_min_warp(rP);
+                if (MODE != MODE_UNIFORM_PROPOSAL) { rS = krec_min_warp<false>(rS); rV = krec_min_warp<false>(rV); }
+                if (MODE != MODE_BEST_ALL) rP = krec_min_warp<MODE == MODE_UNIFORM_ALL>(rP);
 #pragma unroll
                 for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, m);
                 if (lane == 0) {
@@ -504,7 +558,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 }
             }
         }
+        PROF_MARK(3);
         cluster.sync();
+        PROF_MARK(4);
         // ---- leader: best tracking, Eq. 7, termination
         if (leader) {
             KRec S = krec_none(), V = krec_none(), P = krec_none();
@@ -539,7 +595,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                     ck1 = sp.sla ? 0u : 1u; ck2 = okey(sp.h); cidx = P.idx;
                 } else {
                     evals += (long long)total;
-                    if (S.idx != 0x7FFFFFFFFFFFFFFFLL) { ck1 = 0u; ck2 = S.key; cidx = S.idx; }
+                    if (S.idx != 0x7FFFFFFF) { ck1 = 0u; ck2 = S.key; cidx = S.idx; }
                     else { ck1 = 1u; ck2 = V.key; cidx = V.idx; }
                     if (MODE == MODE_BEST_ALL) {
                         const KRec &B = krec_less(S.key, S.idx, V) ? S : V;   // min h overall
@@ -586,7 +642,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             s.dec_move = mv;
             s.dec_done = fin;
         }
+        PROF_MARK(5);
         cluster.sync();
+        PROF_MARK(6);
         if (tid == 0) {
             long long mv;
             int dn;
@@ -600,10 +658,13 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         }
         __syncthreads();
         done = s.dec_done;
+        PROF_MARK(7);
     }
     // No CTA may leave while a peer can still read its shared memory over DSMEM
     // (the non-leaders read the leader's decision after the last step).
     cluster.sync();
+    if (PROF && threadIdx.x == 0 && args.prof)
+        for (int q = 0; q < 7; ++q) args.prof[((size_t)blockIdx.x) * 8 + q] = prof_acc[q];
 
     if (leader) {
         clv_chain_result r;
@@ -627,9 +688,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     }
 }
 
-template <int MODE, int MINB, int UNR>
+template <int MODE, int MINB, int UNR, bool PROF = false>
 static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
-    auto kern = anneal_kernel<MODE, MINB, UNR>;
+    auto kern = anneal_kernel<MODE, MINB, UNR, PROF>;
     const size_t smem = sizeof(AnnealSmem) + sizeof(RemEnt) * (size_t)(a.E * (a.E + 1) / 2);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -673,9 +734,10 @@ cudaError_t launch_anneal(const AnnealArgs &a, int cluster_size, cudaStream_t st
     if (a.proposal == 0) {
         // tuning variants of the headline mode (CLV_ANNEAL_VARIANT, default 0)
         switch (env_int("CLV_ANNEAL_VARIANT", 0)) {
-            case 1: return launch_mode<MODE_BEST_ALL, 3, 2>(a, cluster_size, st);
+            case 1: return launch_mode<MODE_BEST_ALL, 3, 1>(a, cluster_size, st);
             case 2: return launch_mode<MODE_BEST_ALL, 4, 1>(a, cluster_size, st);
-            case 3: return launch_mode<MODE_BEST_ALL, 2, 2>(a, cluster_size, st);
+            case 3: return launch_mode<MODE_BEST_ALL, 2, 1>(a, cluster_size, st);
+            case 9: return launch_mode<MODE_BEST_ALL, 3, 1, true>(a, cluster_size, st);
             default: return launch_mode<MODE_BEST_ALL, 3, 1>(a, cluster_size, st);
         }
     }

@@ -148,6 +148,9 @@ int fetch_best(clv_ctx *ctx, int mode, cudaStream_t st, clv_best *best) {
 
 }  // namespace
 
+static long long *prof_buf = nullptr;   // debug phase profile (CLV_ANNEAL_VARIANT=9)
+static size_t prof_cap = 0;
+
 extern "C" {
 
 int clv_abi_version(void) { return CLV_ABI_VERSION; }
@@ -584,8 +587,24 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
     a.stall_limit = ap->stall_limit; a.max_steps = ap->max_steps; a.proposal = ap->proposal; a.evaluate = ap->evaluate;
     a.n = n; a.n_chains = n_chains; a.E = ctx->fam[family].E; a.chain_base = chain_base; a.seed = seed;
     a.start_w = start_w_dev; a.res = results_dev; a.best_w = best_w_dev; a.final_w = final_w_dev; a.log = log_dev;
+    {
+        // debug phase profile buffer (CLV_ANNEAL_VARIANT=9 only)
+        const char *v = getenv("CLV_ANNEAL_VARIANT");
+        if (v && atoi(v) == 9) {
+            size_t need = (size_t)n_chains * 16 * 8;
+            if (prof_cap < need) { cudaFree(prof_buf); cudaMalloc(&prof_buf, need * sizeof(long long)); prof_cap = need; }
+            cudaMemsetAsync(prof_buf, 0, need * sizeof(long long), st);
+            a.prof = prof_buf;
+        }
+    }
     CLV_CUDA(launch_anneal(a, cluster_size, st), "anneal");
     return CLV_OK;
+}
+
+// debug: copy the last phase profile (CLV_ANNEAL_VARIANT=9) -- not part of the public ABI
+int clv_debug_anneal_profile(long long *host, size_t count) {
+    if (!prof_buf || count > prof_cap) return CLV_ERR_NOT_READY;
+    return cudaMemcpy(host, prof_buf, count * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? CLV_OK : CLV_ERR_CUDA;
 }
 
 int clv_select_chains(clv_ctx *ctx, const clv_chain_result *res, int n_chains, int64_t chain_base,

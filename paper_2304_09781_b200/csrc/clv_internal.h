@@ -138,6 +138,7 @@ struct AnnealArgs {
     uint16_t *best_w;
     uint16_t *final_w;
     clv_log_row *log;
+    long long *prof;                // optional phase profile (debug variant only)
 };
 
 struct ScoreArgs {

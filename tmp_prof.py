@@ -1,0 +1,20 @@
+import sys; sys.path.insert(0,'.')
+import numpy as np, torch, time, ctypes, os
+from paper_2304_09781_b200.engine import CloverEngine
+from paper_2304_09781_b200.profiles import synthetic_profile
+from paper_2304_09781_b200.objective import AnnealParams
+from paper_2304_09781_b200 import _native as N
+import bench
+eng=CloverEngine(n_max=64); prof=synthetic_profile('efficientnet')
+sc=eng.calibrate(prof,64,350.0,0.5)
+st=bench.make_starts(eng,prof,bench.SEED,0,128)
+ap=AnnealParams(max_steps=64)
+lib=N.load(); lib.clv_debug_anneal_profile.argtypes=[ctypes.c_void_p, ctypes.c_size_t]
+for cl in (3,):
+    b=eng.anneal(st,prof,sc,ap,1,cluster=cl); torch.cuda.synchronize()
+    nb=len(st)*cl
+    buf=np.zeros(nb*8,dtype=np.int64); lib.clv_debug_anneal_profile(buf.ctypes.data, nb*8)
+    buf=buf.reshape(len(st),cl,8)[:,:,:7]
+    names=["prepare","score","cta_reduce","sync1","leader","sync2","apply"]
+    lead=buf[:,0,:].mean(0)/64; other=buf[:,1,:].mean(0)/64
+    print("cluster",cl,"cycles/step leader:", {k:int(v) for k,v in zip(names,lead)}, "\n  rank1:", {k:int(v) for k,v in zip(names,other)})
