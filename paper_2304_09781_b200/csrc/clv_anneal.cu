@@ -20,6 +20,7 @@
 // broadcasts the accepted move, which every CTA applies to its own centre.
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <math_constants.h>
 #include "clv_internal.h"
 
 namespace cg = cooperative_groups;
@@ -104,6 +105,9 @@ struct __align__(16) AnnealSmem {
     int fsvec[CLV_K];                      // slice vector the feasibility bytes belong to
     unsigned char feasS[25];
     unsigned char feasD[625];
+    // per-warp queues of screening survivors (removal index, list entry)
+    unsigned short qj[NWARP][64];
+    uint32_t qe[NWARP][64];
     // reduction
     KRec wS[NWARP], wV[NWARP], wP[NWARP];
     unsigned long long wc[NWARP];
@@ -304,7 +308,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, const Fa
 enum { EC_RQ = 0, EC_ENS, EC_IDLES, EC_I3600R, EC_RSAT, EC_AB, EC_KA, EC_KC, EC_LAM, EC_SLO, EC_STRICT };
 
 __device__ __forceinline__ bool screen_out(const AnnealSmem &s, float t, float ac, float en, float id, float lmax,
-                                           const KRec &rS, const KRec &rV) {
+                                           double bS, double bV) {
     const float *c = s.ecf;
     const float inv = __frcp_rn(t);
     const float A = ac * inv;
@@ -323,16 +327,31 @@ __device__ __forceinline__ bool screen_out(const AnnealSmem &s, float t, float a
     const float relL = 4e-6f * (2.0f + __frcp_rn(den));
     const float slo = c[EC_SLO];
     if (L * (1.0f + relL) < slo) {                       // SLA surely met: h = -f
-        return rS.key != ~0ULL && (double)(-f - M) > rS.hv;
+        return (double)(-f - M) > bS;
     }
     if (L * (1.0f - relL) > slo && fabsf(f) > M) {       // SLA surely violated, sign of f sure
         const bool soft = f >= 0.0f || c[EC_STRICT] != 0.0f;
         const float q = soft ? slo * __frcp_rn(L) : L * __frcp_rn(slo);
         const float h = -f * q;
         const float err = 1.01f * q * (M + fabsf(f) * 2.0f * relL) + 1e-6f * fabsf(h);
-        return rV.key != ~0ULL && (double)(h - err) > rV.hv;
+        return (double)(h - err) > bV;
     }
     return false;
+}
+
+// Exact score of one double move + record update (the compacted survivors).
+template <int MODE>
+__device__ __forceinline__ void exact_pair(const AnnealSmem &s, const RemEnt &R, uint32_t ent, int idx, KRec &rS,
+                                           KRec &rV) {
+    const int a1 = ent & 63, a2 = (ent >> 6) & 63;
+    const unsigned long long m = R.mR | s.rbit[a1] | s.rbit[a2];
+    const ARow &A1 = s.row[a1], &A2 = s.row[a2];
+    const Score sc = epilogue_d(s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
+                                s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
+                                s.lat_by_rank[63 - __clzll((long long)m)], s.ec);
+    const unsigned long long key = okey(sc.h);
+    if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; rS.hv = sc.h; } }
+    else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; rV.hv = sc.h; } }
 }
 
 template <int MODE, bool PAIR>
@@ -359,7 +378,8 @@ __device__ __forceinline__ void consider(const AnnealSmem &s, const RemEnt &R, i
             const float4 y = s.rowf[a2];
             t += y.x; ac += y.y; en += y.z; id += y.w;
         }
-        if (screen_out(s, t, ac, en, id, s.latf_by_rank[top], rS, rV)) return;
+        if (screen_out(s, t, ac, en, id, s.latf_by_rank[top], rS.key != ~0ULL ? rS.hv : CUDART_INF,
+                       rV.key != ~0ULL ? rV.hv : CUDART_INF)) return;
     }
     const ARow &A1 = s.row[a1];
     double t = s.S[0] + R.d0 + A1.thr, ac = s.S[1] + R.d1 + A1.acc, en = s.S[2] + R.d2 + A1.en,
@@ -503,7 +523,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (a >= E) { a -= E; ++i; }
             }
         }
-        // ---- doubles: (removal pair j, static move-list entry); warp-contiguous chunks
+        // ---- doubles: (removal pair j, static move-list entry); warp-contiguous chunks.
+        // MODE_BEST_ALL screens every candidate in fp32 and queues the survivors per
+        // warp, so the exact fp64 scoring runs on full, converged warps.
         {
             const int lane = tid & 31, wid = tid >> 5;
             const int ND = s.nLen;
@@ -511,29 +533,87 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             const int W = CL * NWARP;
             const int chunk = (((ND + W - 1) / W) + 31) & ~31;
             const int gw = crank * NWARP + wid;
-            int t = gw * chunk + lane;
-            const int tend = min(gw * chunk + chunk, ND);
-            if (gw * chunk < ND) {
+            const int tb0 = gw * chunk;
+            const int tend = min(tb0 + chunk, ND);
+            if (tb0 < ND) {
                 int lo = 0, hi = s.nRP - 1;
-                const int t0 = t < ND ? t : ND - 1;
+                const int t0 = min(tb0 + lane, ND - 1);
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
                     if (rp[mid].pre <= t0) lo = mid; else hi = mid - 1;
                 }
                 int j = lo;
                 const uint32_t *plist = T.pair_list;
-                for (; t < tend; t += 32) {
-                    while (t >= rp[j].pre + rp[j].len) ++j;
-                    const RemEnt &R = rp[j];
-                    const uint32_t ent = __ldg(plist + R.off + (t - R.pre));
-                    if (s.feasD[R.code + ((ent >> 12) & 31)]) {
-                        ++cnt;
-                        consider<MODE, true>(s, R, ent & 63, (ent >> 6) & 63, E * E + (int)R.p * NPc + (int)(ent >> 17),
-                                             rS, rV, rP, args.seed, gchain, (uint64_t)k);
+                if (MODE == MODE_BEST_ALL) {
+                    double bS = CUDART_INF, bV = CUDART_INF;      // warp-wide screening bounds
+                    int qn = 0;
+                    for (int tb = tb0; tb < tend; tb += 32) {
+                        const int t = tb + lane;
+                        bool surv = false;
+                        uint32_t ent = 0;
+                        if (t < tend) {
+                            while (t >= rp[j].pre + rp[j].len) ++j;
+                            const RemEnt &R = rp[j];
+                            ent = __ldg(plist + R.off + (t - R.pre));
+                            if (s.feasD[R.code + ((ent >> 12) & 31)]) {
+                                ++cnt;
+                                const int a1 = ent & 63, a2 = (ent >> 6) & 63;
+                                const float4 x = s.rowf[a1], y = s.rowf[a2];
+                                const unsigned long long m = R.mR | s.rbit[a1] | s.rbit[a2];
+                                surv = !screen_out(s, s.Sf[0] + R.f0 + x.x + y.x, s.Sf[1] + R.f1 + x.y + y.y,
+                                                   s.Sf[2] + R.f2 + x.z + y.z, s.Sf[3] + R.f3 + x.w + y.w,
+                                                   s.latf_by_rank[63 - __clzll((long long)m)], bS, bV);
+                            }
+                        }
+                        const unsigned bal = __ballot_sync(0xFFFFFFFFu, surv);
+                        if (surv) {
+                            const int pos = qn + __popc(bal & ((1u << lane) - 1u));
+                            s.qj[wid][pos] = (unsigned short)j;
+                            s.qe[wid][pos] = ent;
+                        }
+                        qn += __popc(bal);
+                        if (qn >= 32) {
+                            __syncwarp();
+                            const int jj = s.qj[wid][lane];
+                            const uint32_t ee = s.qe[wid][lane];
+                            const RemEnt &R = rp[jj];
+                            exact_pair<MODE>(s, R, ee, E * E + (int)R.p * NPc + (int)(ee >> 17), rS, rV);
+                            qn -= 32;
+                            __syncwarp();
+                            if (lane < qn) { s.qj[wid][lane] = s.qj[wid][lane + 32]; s.qe[wid][lane] = s.qe[wid][lane + 32]; }
+                            __syncwarp();
+                            double mS = rS.key != ~0ULL ? rS.hv : CUDART_INF, mV = rV.key != ~0ULL ? rV.hv : CUDART_INF;
+#pragma unroll
+                            for (int o = 16; o >= 1; o >>= 1) {
+                                mS = fmin(mS, __shfl_xor_sync(0xFFFFFFFFu, mS, o));
+                                mV = fmin(mV, __shfl_xor_sync(0xFFFFFFFFu, mV, o));
+                            }
+                            bS = mS; bV = mV;
+                        }
+                    }
+                    __syncwarp();
+                    if (lane < qn) {
+                        const int jj = s.qj[wid][lane];
+                        const uint32_t ee = s.qe[wid][lane];
+                        const RemEnt &R = rp[jj];
+                        exact_pair<MODE>(s, R, ee, E * E + (int)R.p * NPc + (int)(ee >> 17), rS, rV);
+                    }
+                    __syncwarp();
+                } else {
+                    for (int t = tb0 + lane; t < tend; t += 32) {
+                        while (t >= rp[j].pre + rp[j].len) ++j;
+                        const RemEnt &R = rp[j];
+                        const uint32_t ent = __ldg(plist + R.off + (t - R.pre));
+                        if (s.feasD[R.code + ((ent >> 12) & 31)]) {
+                            ++cnt;
+                            consider<MODE, true>(s, R, ent & 63, (ent >> 6) & 63, E * E + (int)R.p * NPc + (int)(ent >> 17),
+                                                 rS, rV, rP, args.seed, gchain, (uint64_t)k);
+                        }
                     }
                 }
             }
         }
+        PROF_MARK(2);
         // ---- CTA reduction, then DSMEM publish into the leader's slots
         {
             const int lane = tid & 31, wid = tid >> 5;
