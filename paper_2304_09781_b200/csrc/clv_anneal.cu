@@ -82,7 +82,7 @@ struct __align__(16) AnnealSmem {
     double lat_by_rank[CLV_MAX_EDGES];
     float latf_by_rank[CLV_MAX_EDGES];
     float Sf[4];                           // fp32 copy of the centre sums
-    float ecf[12];                         // fp32 epilogue constants (screening only)
+    float ecf[16];                         // fp32 screening constants (EC_*)
     unsigned long long rbit[CLV_MAX_EDGES];
     unsigned long long adjm[CLV_MAX_EDGES];
     EvalConst ec;
@@ -305,36 +305,37 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, const Fa
 // would become the proposal).  Records are exact minima of the exactly scored
 // candidates, and a skipped candidate is provably worse than a scored one, so the
 // selection is bit-identical to scoring everything.
-enum { EC_RQ = 0, EC_ENS, EC_IDLES, EC_I3600R, EC_RSAT, EC_AB, EC_KA, EC_KC, EC_LAM, EC_SLO, EC_STRICT };
+enum { EC_RQ = 0, EC_ENS, EC_IDLE, EC_RSAT, EC_C0, EC_C1, EC_C2, EC_SLO, EC_RSLO, EC_STRICT, EC_MAG, EC_N };
 
-__device__ __forceinline__ bool screen_out(const AnnealSmem &s, float t, float ac, float en, float id, float lmax,
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// fp32 estimate of (f, L) with error bounds; true when the candidate provably cannot
+// beat the bound of its SLA class (bS: SLA-meeting, bV: violating).
+//   f = c0 + c1*E + c2*A  with c0 = 100*lam - (1-lam)*A_base*kA, c1 = -lam*kC, c2 = (1-lam)*kA
+// The bound M ~ 2^-14 of the magnitudes covers fp32 rounding of the sums (<= 2.4e-7
+// relative), of rcp.approx (<= 1 ulp) and of every product (~1e-6 total).
+__device__ __forceinline__ bool screen_out(const float *c, float t, float ac, float en, float id, float lmax,
                                            double bS, double bV) {
-    const float *c = s.ecf;
-    const float inv = __frcp_rn(t);
+    const float inv = rcp_approx(t);
     const float A = ac * inv;
     const float rho = c[EC_RQ] * inv;
-    const float e = (en * inv) * c[EC_ENS];
-    const float rc = fminf(rho, 1.0f);
-    const float E = e + ((1.0f - rc) * (id * c[EC_IDLES])) * c[EC_I3600R];
-    const float rq = fminf(rho, c[EC_RSAT]);
-    const float den = 1.0f - rq;
-    const float L = lmax * __frcp_rn(den);
-    const float EkC = E * c[EC_KC];
-    const float dA = (A - c[EC_AB]) * c[EC_KA];
-    const float f = c[EC_LAM] * (100.0f - EkC) + (1.0f - c[EC_LAM]) * dA;
-    // absolute error bound of f (~8x the worst-case fp32 propagation) and relative bound of L
-    const float M = 4e-6f * (100.0f + fabsf(EkC) + (A + c[EC_AB]) * c[EC_KA]);
-    const float relL = 4e-6f * (2.0f + __frcp_rn(den));
+    const float E = __fmaf_rn((1.0f - fminf(rho, 1.0f)) * id, c[EC_IDLE], (en * inv) * c[EC_ENS]);
+    const float rx = rcp_approx(1.0f - fminf(rho, c[EC_RSAT]));
+    const float L = lmax * rx;
+    const float tE = c[EC_C1] * E, tA = c[EC_C2] * A;
+    const float f = c[EC_C0] + tE + tA;
+    const float M = 6.1e-5f * (c[EC_MAG] + fabsf(tE) + fabsf(tA));
+    const float relL = 4e-6f * (2.0f + rx);
     const float slo = c[EC_SLO];
-    if (L * (1.0f + relL) < slo) {                       // SLA surely met: h = -f
-        return (double)(-f - M) > bS;
-    }
-    if (L * (1.0f - relL) > slo && fabsf(f) > M) {       // SLA surely violated, sign of f sure
-        const bool soft = f >= 0.0f || c[EC_STRICT] != 0.0f;
-        const float q = soft ? slo * __frcp_rn(L) : L * __frcp_rn(slo);
+    if (L * (1.0f + relL) < slo) return (double)(-f - M) > bS;        // SLA surely met: h = -f
+    if (L * (1.0f - relL) > slo && fabsf(f) > M) {                   // surely violated, sign of f sure
+        const float q = (f >= 0.0f || c[EC_STRICT] != 0.0f) ? slo * rcp_approx(L) : L * c[EC_RSLO];
         const float h = -f * q;
-        const float err = 1.01f * q * (M + fabsf(f) * 2.0f * relL) + 1e-6f * fabsf(h);
-        return (double)(h - err) > bV;
+        return (double)(h - 1.02f * q * (M + fabsf(f) * 2.0f * relL) - 1e-5f * fabsf(h)) > bV;
     }
     return false;
 }
@@ -342,13 +343,18 @@ __device__ __forceinline__ bool screen_out(const AnnealSmem &s, float t, float a
 // Exact score of one double move + record update (the compacted survivors).
 template <int MODE>
 __device__ __forceinline__ void exact_pair(const AnnealSmem &s, const RemEnt &R, uint32_t ent, int idx, KRec &rS,
-                                           KRec &rV) {
+                                           KRec &rV, bool pair = true) {
     const int a1 = ent & 63, a2 = (ent >> 6) & 63;
-    const unsigned long long m = R.mR | s.rbit[a1] | s.rbit[a2];
-    const ARow &A1 = s.row[a1], &A2 = s.row[a2];
-    const Score sc = epilogue_d(s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
-                                s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
-                                s.lat_by_rank[63 - __clzll((long long)m)], s.ec);
+    const ARow &A1 = s.row[a1];
+    double t = s.S[0] + R.d0 + A1.thr, ac = s.S[1] + R.d1 + A1.acc, en = s.S[2] + R.d2 + A1.en,
+           id = s.S[3] + R.d3 + A1.idle;
+    unsigned long long m = R.mR | s.rbit[a1];
+    if (pair) {
+        const ARow &A2 = s.row[a2];
+        t += A2.thr; ac += A2.acc; en += A2.en; id += A2.idle;
+        m |= s.rbit[a2];
+    }
+    const Score sc = epilogue_d(t, ac, en, id, s.lat_by_rank[63 - __clzll((long long)m)], s.ec);
     const unsigned long long key = okey(sc.h);
     if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; rS.hv = sc.h; } }
     else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; rV.hv = sc.h; } }
@@ -378,7 +384,7 @@ __device__ __forceinline__ void consider(const AnnealSmem &s, const RemEnt &R, i
             const float4 y = s.rowf[a2];
             t += y.x; ac += y.y; en += y.z; id += y.w;
         }
-        if (screen_out(s, t, ac, en, id, s.latf_by_rank[top], rS.key != ~0ULL ? rS.hv : CUDART_INF,
+        if (screen_out(s.ecf, t, ac, en, id, s.latf_by_rank[top], rS.key != ~0ULL ? rS.hv : CUDART_INF,
                        rV.key != ~0ULL ? rV.hv : CUDART_INF)) return;
     }
     const ARow &A1 = s.row[a1];
@@ -408,6 +414,7 @@ template <int MODE, int MINB, int UNR, bool PROF = false>
 __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
     long long prof_acc[7] = {0, 0, 0, 0, 0, 0, 0};
     long long prof_last = 0;
+    long long prof_surv = 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     AnnealSmem &s = *reinterpret_cast<AnnealSmem *>(smem_raw);
     RemEnt *const rp = reinterpret_cast<RemEnt *>(smem_raw + sizeof(AnnealSmem));   // dynamic tail, E(E+1)/2
@@ -446,10 +453,12 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         s.mem_ok = T.mem_ok;
         s.ec = args.ec[args.n_ec == 1 ? 0 : chain];
         const EvalConst &c = s.ec;
-        s.ecf[EC_RQ] = (float)c.R_q; s.ecf[EC_ENS] = (float)c.en_scale; s.ecf[EC_IDLES] = (float)c.idle_scale;
-        s.ecf[EC_I3600R] = (float)c.inv_3600R; s.ecf[EC_RSAT] = (float)c.rho_sat; s.ecf[EC_AB] = (float)c.a_base;
-        s.ecf[EC_KA] = (float)c.kA; s.ecf[EC_KC] = (float)c.kC; s.ecf[EC_LAM] = (float)c.lam;
-        s.ecf[EC_SLO] = (float)c.slo; s.ecf[EC_STRICT] = (float)c.strict;
+        const double c0 = 100.0 * c.lam - (1.0 - c.lam) * c.a_base * c.kA;
+        s.ecf[EC_RQ] = (float)c.R_q; s.ecf[EC_ENS] = (float)c.en_scale;
+        s.ecf[EC_IDLE] = (float)(c.idle_scale * c.inv_3600R); s.ecf[EC_RSAT] = (float)c.rho_sat;
+        s.ecf[EC_C0] = (float)c0; s.ecf[EC_C1] = (float)(-c.lam * c.kC); s.ecf[EC_C2] = (float)((1.0 - c.lam) * c.kA);
+        s.ecf[EC_SLO] = (float)c.slo; s.ecf[EC_RSLO] = (float)(1.0 / c.slo); s.ecf[EC_STRICT] = (float)c.strict;
+        s.ecf[EC_MAG] = (float)(fabs(100.0 * c.lam) + fabs((1.0 - c.lam) * c.a_base * c.kA));
     }
     __syncthreads();
     if (tid == 0) {
@@ -507,99 +516,146 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         PROF_MARK(1);
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
         unsigned long long cnt = 0;
-        // ---- singles: (present edge i, target edge a)
-        {
-            const int nS = s.nPE * E;
-            int i = gt / E, a = gt - (gt / E) * E;
-            const int dI = G / E, dA = G - (G / E) * E;
-            for (int t = gt; t < nS; t += G) {
-                const RemEnt &R = s.se[i];
-                const bool ok = (a != R.r1) && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]];
-                if (ok) {
-                    ++cnt;
-                    consider<MODE, false>(s, R, a, 0, (int)(R.p * E + a), rS, rV, rP, args.seed, gchain, (uint64_t)k);
-                }
-                i += dI; a += dA;
-                if (a >= E) { a -= E; ++i; }
-            }
-        }
-        // ---- doubles: (removal pair j, static move-list entry); warp-contiguous chunks.
-        // MODE_BEST_ALL screens every candidate in fp32 and queues the survivors per
-        // warp, so the exact fp64 scoring runs on full, converged warps.
-        {
+        if (MODE == MODE_BEST_ALL) {
+            // fp32 screen of every neighbour, survivors queued per warp and scored exactly
+            // (fp64) in full warps.  Work unit = one removal entry (warp-uniform), lanes
+            // stride its target list; entries are split over the cluster's warps by the
+            // prefix of their list lengths.
             const int lane = tid & 31, wid = tid >> 5;
-            const int ND = s.nLen;
             const int NPc = E * (E + 1) / 2;
             const int W = CL * NWARP;
-            const int chunk = (((ND + W - 1) / W) + 31) & ~31;
             const int gw = crank * NWARP + wid;
-            const int tb0 = gw * chunk;
-            const int tend = min(tb0 + chunk, ND);
-            if (tb0 < ND) {
-                int lo = 0, hi = s.nRP - 1;
-                const int t0 = min(tb0 + lane, ND - 1);
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (rp[mid].pre <= t0) lo = mid; else hi = mid - 1;
-                }
-                int j = lo;
-                const uint32_t *plist = T.pair_list;
-                if (MODE == MODE_BEST_ALL) {
-                    double bS = CUDART_INF, bV = CUDART_INF;      // warp-wide screening bounds
-                    int qn = 0;
-                    for (int tb = tb0; tb < tend; tb += 32) {
-                        const int t = tb + lane;
-                        bool surv = false;
-                        uint32_t ent = 0;
-                        if (t < tend) {
-                            while (t >= rp[j].pre + rp[j].len) ++j;
-                            const RemEnt &R = rp[j];
-                            ent = __ldg(plist + R.off + (t - R.pre));
-                            if (s.feasD[R.code + ((ent >> 12) & 31)]) {
-                                ++cnt;
-                                const int a1 = ent & 63, a2 = (ent >> 6) & 63;
-                                const float4 x = s.rowf[a1], y = s.rowf[a2];
-                                const unsigned long long m = R.mR | s.rbit[a1] | s.rbit[a2];
-                                surv = !screen_out(s, s.Sf[0] + R.f0 + x.x + y.x, s.Sf[1] + R.f1 + x.y + y.y,
-                                                   s.Sf[2] + R.f2 + x.z + y.z, s.Sf[3] + R.f3 + x.w + y.w,
-                                                   s.latf_by_rank[63 - __clzll((long long)m)], bS, bV);
-                            }
-                        }
-                        const unsigned bal = __ballot_sync(0xFFFFFFFFu, surv);
-                        if (surv) {
-                            const int pos = qn + __popc(bal & ((1u << lane) - 1u));
-                            s.qj[wid][pos] = (unsigned short)j;
-                            s.qe[wid][pos] = ent;
-                        }
-                        qn += __popc(bal);
-                        if (qn >= 32) {
-                            __syncwarp();
-                            const int jj = s.qj[wid][lane];
-                            const uint32_t ee = s.qe[wid][lane];
-                            const RemEnt &R = rp[jj];
-                            exact_pair<MODE>(s, R, ee, E * E + (int)R.p * NPc + (int)(ee >> 17), rS, rV);
-                            qn -= 32;
-                            __syncwarp();
-                            if (lane < qn) { s.qj[wid][lane] = s.qj[wid][lane + 32]; s.qe[wid][lane] = s.qe[wid][lane + 32]; }
-                            __syncwarp();
-                            double mS = rS.key != ~0ULL ? rS.hv : CUDART_INF, mV = rV.key != ~0ULL ? rV.hv : CUDART_INF;
-#pragma unroll
-                            for (int o = 16; o >= 1; o >>= 1) {
-                                mS = fmin(mS, __shfl_xor_sync(0xFFFFFFFFu, mS, o));
-                                mV = fmin(mV, __shfl_xor_sync(0xFFFFFFFFu, mV, o));
-                            }
-                            bS = mS; bV = mV;
-                        }
-                    }
-                    __syncwarp();
-                    if (lane < qn) {
-                        const int jj = s.qj[wid][lane];
-                        const uint32_t ee = s.qe[wid][lane];
+            double bS = CUDART_INF, bV = CUDART_INF;
+            int qn = 0;
+            const float *ecf = s.ecf;
+            const float S0 = s.Sf[0], S1 = s.Sf[1], S2 = s.Sf[2], S3 = s.Sf[3];
+            auto drain = [&](int nq) {            // exact-score queue entries [0, nq) (nq <= 32)
+                __syncwarp();
+                if (lane < nq) {
+                    const int jj = s.qj[wid][lane];
+                    const uint32_t ee = s.qe[wid][lane];
+                    if (jj & 0x8000) {
+                        const RemEnt &R = s.se[jj & 0x7FFF];
+                        exact_pair<MODE>(s, R, ee, (int)R.p * E + (int)(ee & 63), rS, rV, false);
+                    } else {
                         const RemEnt &R = rp[jj];
-                        exact_pair<MODE>(s, R, ee, E * E + (int)R.p * NPc + (int)(ee >> 17), rS, rV);
+                        exact_pair<MODE>(s, R, ee, E * E + (int)R.p * NPc + (int)(ee >> 17), rS, rV, true);
                     }
+                }
+                __syncwarp();
+            };
+            auto push = [&](bool surv, int jtag, uint32_t ent) {
+                const unsigned bal = __ballot_sync(0xFFFFFFFFu, surv);
+                if (surv) {
+                    const int pos = qn + __popc(bal & ((1u << lane) - 1u));
+                    s.qj[wid][pos] = (unsigned short)jtag;
+                    s.qe[wid][pos] = ent;
+                }
+                qn += __popc(bal);
+                if (PROF) prof_surv += (lane == 0) ? __popc(bal) : 0;
+                if (qn >= 32) {
+                    drain(32);
+                    qn -= 32;
+                    if (lane < qn) { s.qj[wid][lane] = s.qj[wid][lane + 32]; s.qe[wid][lane] = s.qe[wid][lane + 32]; }
+                    double mS = rS.key != ~0ULL ? rS.hv : CUDART_INF, mV = rV.key != ~0ULL ? rV.hv : CUDART_INF;
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) {
+                        mS = fmin(mS, __shfl_xor_sync(0xFFFFFFFFu, mS, o));
+                        mV = fmin(mV, __shfl_xor_sync(0xFFFFFFFFu, mV, o));
+                    }
+                    bS = mS; bV = mV;
                     __syncwarp();
-                } else {
+                }
+            };
+            // singles: present edge i (warp-uniform), lanes over targets a
+            for (int i = gw; i < s.nPE; i += W) {
+                const RemEnt &R = s.se[i];
+                for (int a0 = 0; a0 < E; a0 += 32) {
+                    const int a = a0 + lane;
+                    bool surv = false;
+                    if (a < E && a != R.r1 && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]]) {
+                        ++cnt;
+                        const float4 x = s.rowf[a];
+                        surv = !screen_out(ecf, S0 + R.f0 + x.x, S1 + R.f1 + x.y, S2 + R.f2 + x.z, S3 + R.f3 + x.w,
+                                           s.latf_by_rank[63 - __clzll((long long)(R.mR | s.rbit[a]))], bS, bV);
+                    }
+                    push(surv, 0x8000 | i, (uint32_t)a);
+                }
+            }
+            // doubles: warp gets the removal entries whose list prefix falls in its chunk
+            {
+                const int ND = s.nLen;
+                const int chunk = (ND + W - 1) / W;
+                const int lo_t = gw * chunk, hi_t = min(lo_t + chunk, ND);
+                if (lo_t < hi_t) {
+                    int lo = 0, hi = s.nRP;                  // first entry with pre >= lo_t
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (rp[mid].pre < lo_t) lo = mid + 1; else hi = mid;
+                    }
+                    const uint32_t *plist = T.pair_list;
+                    for (int j = lo; j < s.nRP && rp[j].pre < hi_t; ++j) {
+                        const RemEnt &R = rp[j];
+                        const int len = R.len;
+                        const uint32_t *lst = plist + R.off;
+                        for (int o0 = 0; o0 < len; o0 += 32) {
+                            const int o = o0 + lane;
+                            bool surv = false;
+                            uint32_t ent = 0;
+                            if (o < len) {
+                                ent = __ldg(lst + o);
+                                if (s.feasD[R.code + ((ent >> 12) & 31)]) {
+                                    ++cnt;
+                                    const int a1 = ent & 63, a2 = (ent >> 6) & 63;
+                                    const float4 x = s.rowf[a1], y = s.rowf[a2];
+                                    surv = !screen_out(ecf, S0 + R.f0 + x.x + y.x, S1 + R.f1 + x.y + y.y,
+                                                       S2 + R.f2 + x.z + y.z, S3 + R.f3 + x.w + y.w,
+                                                       s.latf_by_rank[63 - __clzll((long long)(R.mR | s.rbit[a1] | s.rbit[a2]))],
+                                                       bS, bV);
+                                }
+                            }
+                            push(surv, j, ent);
+                        }
+                    }
+                }
+            }
+            drain(qn);
+        } else {
+            // ---- singles: (present edge i, target edge a)
+            {
+                const int nS = s.nPE * E;
+                int i = gt / E, a = gt - (gt / E) * E;
+                const int dI = G / E, dA = G - (G / E) * E;
+                for (int t = gt; t < nS; t += G) {
+                    const RemEnt &R = s.se[i];
+                    const bool ok = (a != R.r1) && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]];
+                    if (ok) {
+                        ++cnt;
+                        consider<MODE, false>(s, R, a, 0, (int)(R.p * E + a), rS, rV, rP, args.seed, gchain, (uint64_t)k);
+                    }
+                    i += dI; a += dA;
+                    if (a >= E) { a -= E; ++i; }
+                }
+            }
+            // ---- doubles: flattened move space, warp-contiguous chunks
+            {
+                const int lane = tid & 31, wid = tid >> 5;
+                const int ND = s.nLen;
+                const int NPc = E * (E + 1) / 2;
+                const int W = CL * NWARP;
+                const int chunk = (((ND + W - 1) / W) + 31) & ~31;
+                const int gw = crank * NWARP + wid;
+                const int tb0 = gw * chunk;
+                const int tend = min(tb0 + chunk, ND);
+                if (tb0 < ND) {
+                    int lo = 0, hi = s.nRP - 1;
+                    const int t0 = min(tb0 + lane, ND - 1);
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (rp[mid].pre <= t0) lo = mid; else hi = mid - 1;
+                    }
+                    int j = lo;
+                    const uint32_t *plist = T.pair_list;
                     for (int t = tb0 + lane; t < tend; t += 32) {
                         while (t >= rp[j].pre + rp[j].len) ++j;
                         const RemEnt &R = rp[j];
@@ -745,6 +801,10 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     cluster.sync();
     if (PROF && threadIdx.x == 0 && args.prof)
         for (int q = 0; q < 7; ++q) args.prof[((size_t)blockIdx.x) * 8 + q] = prof_acc[q];
+    if (PROF && args.prof) {                 // survivors of the fp32 screen, summed over the CTA's warps
+        unsigned long long v = (threadIdx.x & 31) == 0 ? (unsigned long long)prof_surv : 0ULL;
+        atomicAdd(reinterpret_cast<unsigned long long *>(args.prof) + ((size_t)blockIdx.x) * 8 + 7, v);
+    }
 
     if (leader) {
         clv_chain_result r;

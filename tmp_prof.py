@@ -14,7 +14,9 @@ for cl in (3,):
     b=eng.anneal(st,prof,sc,ap,1,cluster=cl); torch.cuda.synchronize()
     nb=len(st)*cl
     buf=np.zeros(nb*8,dtype=np.int64); lib.clv_debug_anneal_profile(buf.ctypes.data, nb*8)
-    buf=buf.reshape(len(st),cl,8)[:,:,:7]
+    buf=buf.reshape(len(st),cl,8)
     names=["prepare","score","cta_reduce","sync1","leader","sync2","apply"]
-    lead=buf[:,0,:].mean(0)/64; other=buf[:,1,:].mean(0)/64
+    lead=buf[:,0,:7].mean(0)/64; other=buf[:,1,:7].mean(0)/64
     print("cluster",cl,"cycles/step leader:", {k:int(v) for k,v in zip(names,lead)}, "\n  rank1:", {k:int(v) for k,v in zip(names,other)})
+    ev=b.host()['results']['evals'].sum()
+    print("screen survivors %d of %d candidates (%.3f)"%(buf[:,:,7].sum(), ev, buf[:,:,7].sum()/ev))
