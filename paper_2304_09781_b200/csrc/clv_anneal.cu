@@ -39,16 +39,15 @@ struct __align__(16) ARow {
     double thr, acc, en, idle;
 };
 
-struct __align__(8) RemEnt {            // one removal multiset R (single edge or pair)
-    double d0, d1, d2, d3;                 // -(rows of R), exact integers
-    float f0, f1, f2, f3;                  // the same deltas in fp32 (screening only)
+struct __align__(8) RemEnt {            // one removal multiset R (single edge or pair), 40 B
+    float f0, f1, f2, f3;                  // -(rows of R) in fp32 (screening)
     unsigned long long mR;                 // presence mask (by latency rank) after removal
     int pre;                               // doubles: exclusive prefix of list lengths
     int off;                               // doubles: first entry of the static move list
     unsigned short p;                      // pair index P(r1, r2) (doubles) / edge (singles)
     unsigned short code;                   // slice code of R: sr1*125 + sr2*25 (doubles), sr*5 (singles)
     unsigned char len;                     // doubles: move-list length
-    unsigned char r1, r2;                  // removed edges
+    unsigned char r1, r2;                  // removed edges (r2 = 0xFF for singles)
 };
 
 struct KRec {                              // (key, idx) record; payload hv (uniform proposals)
@@ -246,10 +245,6 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, const Fa
         const bool ok = (x == y) ? (s.w[x] >= 2) : (s.w[x] > 0 && s.w[y] > 0);
         if (!ok) continue;
         RemEnt &r = rp[pos++];
-        r.d0 = -(s.row[x].thr + s.row[y].thr);
-        r.d1 = -(s.row[x].acc + s.row[y].acc);
-        r.d2 = -(s.row[x].en + s.row[y].en);
-        r.d3 = -(s.row[x].idle + s.row[y].idle);
         r.f0 = -(s.rowf[x].x + s.rowf[y].x); r.f1 = -(s.rowf[x].y + s.rowf[y].y);
         r.f2 = -(s.rowf[x].z + s.rowf[y].z); r.f3 = -(s.rowf[x].w + s.rowf[y].w);
         unsigned long long m = s.pmask;
@@ -275,7 +270,6 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, const Fa
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
             if (ok) {
                 RemEnt &r = s.se[c + __popc(bal & ((1u << lane) - 1u))];
-                r.d0 = -s.row[e].thr; r.d1 = -s.row[e].acc; r.d2 = -s.row[e].en; r.d3 = -s.row[e].idle;
                 r.f0 = -s.rowf[e].x; r.f1 = -s.rowf[e].y; r.f2 = -s.rowf[e].z; r.f3 = -s.rowf[e].w;
                 r.mR = (s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask;
                 r.p = (unsigned short)e;
@@ -345,9 +339,13 @@ template <int MODE>
 __device__ __forceinline__ void exact_pair(const AnnealSmem &s, const RemEnt &R, uint32_t ent, int idx, KRec &rS,
                                            KRec &rV, bool pair = true) {
     const int a1 = ent & 63, a2 = (ent >> 6) & 63;
-    const ARow &A1 = s.row[a1];
-    double t = s.S[0] + R.d0 + A1.thr, ac = s.S[1] + R.d1 + A1.acc, en = s.S[2] + R.d2 + A1.en,
-           id = s.S[3] + R.d3 + A1.idle;
+    const ARow &A1 = s.row[a1], &X = s.row[R.r1];
+    double t = s.S[0] - X.thr + A1.thr, ac = s.S[1] - X.acc + A1.acc, en = s.S[2] - X.en + A1.en,
+           id = s.S[3] - X.idle + A1.idle;
+    if (R.r2 != 0xFF) {
+        const ARow &Y = s.row[R.r2];
+        t -= Y.thr; ac -= Y.acc; en -= Y.en; id -= Y.idle;
+    }
     unsigned long long m = R.mR | s.rbit[a1];
     if (pair) {
         const ARow &A2 = s.row[a2];
@@ -387,10 +385,12 @@ __device__ __forceinline__ void consider(const AnnealSmem &s, const RemEnt &R, i
         if (screen_out(s.ecf, t, ac, en, id, s.latf_by_rank[top], rS.key != ~0ULL ? rS.hv : CUDART_INF,
                        rV.key != ~0ULL ? rV.hv : CUDART_INF)) return;
     }
-    const ARow &A1 = s.row[a1];
-    double t = s.S[0] + R.d0 + A1.thr, ac = s.S[1] + R.d1 + A1.acc, en = s.S[2] + R.d2 + A1.en,
-           id = s.S[3] + R.d3 + A1.idle;
+    const ARow &A1 = s.row[a1], &X = s.row[R.r1];
+    double t = s.S[0] - X.thr + A1.thr, ac = s.S[1] - X.acc + A1.acc, en = s.S[2] - X.en + A1.en,
+           id = s.S[3] - X.idle + A1.idle;
     if (PAIR) {
+        const ARow &Y = s.row[R.r2];
+        t -= Y.thr; ac -= Y.acc; en -= Y.en; id -= Y.idle;
         const ARow &A2 = s.row[a2];
         t += A2.thr; ac += A2.acc; en += A2.en; id += A2.idle;
     }
@@ -598,12 +598,14 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                         const RemEnt &R = rp[j];
                         const int len = R.len;
                         const uint32_t *lst = plist + R.off;
+                        uint32_t nxt = lane < len ? __ldg(lst + lane) : 0u;
                         for (int o0 = 0; o0 < len; o0 += 32) {
                             const int o = o0 + lane;
                             bool surv = false;
                             uint32_t ent = 0;
                             if (o < len) {
-                                ent = __ldg(lst + o);
+                                ent = nxt;
+                                if (o + 32 < len) nxt = __ldg(lst + o + 32);
                                 if (s.feasD[R.code + ((ent >> 12) & 31)]) {
                                     ++cnt;
                                     const int a1 = ent & 63, a2 = (ent >> 6) & 63;
