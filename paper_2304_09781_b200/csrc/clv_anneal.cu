@@ -111,8 +111,8 @@ struct __align__(16) AnnealSmem {
     KRec wS[NWARP], wV[NWARP], wP[NWARP];
     unsigned long long wc[NWARP];
     // leader-only slots, one per cluster rank
-    KRec slS[MAXCL], slV[MAXCL], slP[MAXCL];
-    unsigned long long slc[MAXCL];
+    KRec slS[2][MAXCL], slV[2][MAXCL], slP[2][MAXCL];   // [step parity][cluster rank]
+    unsigned long long slc[2][MAXCL];
     long long dec_move;                    // accepted move index, -1 = none
     int dec_done;
     int bw[CLV_MAX_EDGES];
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     unsigned long long bk2 = 0;
     int best_step = -1, stall = 0, steps = 0, status = 0;
     long long best_idx = -1, evals = 1;
-    if (leader) {
+    if (tid == 0) {
         int invalid = 0;
         long long tot = 0;
         for (int e = 0; e < E; ++e) {
@@ -502,9 +502,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         s.dec_done = invalid || (args.max_steps <= 0);
         if (invalid) status = -1;
     }
-    cluster.sync();
-    if (tid == 0 && crank != 0) s.dec_done = *cluster.map_shared_rank(&s.dec_done, 0);
-    __syncthreads();
+    cluster.sync();                          // all CTAs started before any DSMEM traffic
     bool done = s.dec_done;
     const int G = CL * ANT;
     const int gt = crank * ANT + tid;
@@ -690,24 +688,34 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (MODE != MODE_BEST_ALL) rP = krec_min_warp<MODE == MODE_UNIFORM_ALL>(rP);
 #pragma unroll
                 for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, m);
-                if (lane == 0) {
-                    AnnealSmem *ls = cluster.map_shared_rank(&s, 0);
-                    ls->slS[crank] = rS; ls->slV[crank] = rV; ls->slP[crank] = rP; ls->slc[crank] = cnt;
+                // every CTA decides redundantly (identical inputs, deterministic), so the
+                // records go to all CTAs of the cluster -- one cluster barrier per step
+                rS.key = __shfl_sync(0xFFFFFFFFu, rS.key, 0); rS.idx = __shfl_sync(0xFFFFFFFFu, rS.idx, 0);
+                rV.key = __shfl_sync(0xFFFFFFFFu, rV.key, 0); rV.idx = __shfl_sync(0xFFFFFFFFu, rV.idx, 0);
+                rP.key = __shfl_sync(0xFFFFFFFFu, rP.key, 0); rP.idx = __shfl_sync(0xFFFFFFFFu, rP.idx, 0);
+                rP.hv = __shfl_sync(0xFFFFFFFFu, rP.hv, 0);
+                cnt = __shfl_sync(0xFFFFFFFFu, cnt, 0);
+                if (lane < CL) {
+                    AnnealSmem *ls = cluster.map_shared_rank(&s, lane);
+                    const int par = k & 1;
+                    ls->slS[par][crank] = rS; ls->slV[par][crank] = rV; ls->slP[par][crank] = rP;
+                    ls->slc[par][crank] = cnt;
                 }
             }
         }
         PROF_MARK(3);
         cluster.sync();
         PROF_MARK(4);
-        // ---- leader: best tracking, Eq. 7, termination
-        if (leader) {
+        // ---- every CTA (thread 0): best tracking, Eq. 7, termination; rank 0 keeps outputs
+        if (tid == 0) {
+            const int par = k & 1;
             KRec S = krec_none(), V = krec_none(), P = krec_none();
             unsigned long long total = 0;
             for (int q = 0; q < CL; ++q) {
-                if (krec_less(s.slS[q].key, s.slS[q].idx, S)) S = s.slS[q];
-                if (krec_less(s.slV[q].key, s.slV[q].idx, V)) V = s.slV[q];
-                if (krec_less(s.slP[q].key, s.slP[q].idx, P)) P = s.slP[q];
-                total += s.slc[q];
+                if (krec_less(s.slS[par][q].key, s.slS[par][q].idx, S)) S = s.slS[par][q];
+                if (krec_less(s.slV[par][q].key, s.slV[par][q].idx, V)) V = s.slV[par][q];
+                if (krec_less(s.slP[par][q].key, s.slP[par][q].idx, P)) P = s.slP[par][q];
+                total += s.slc[par][q];
             }
             long long mv = NOIDX;
             int fin = 0;
@@ -741,7 +749,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                     } else {
                         pidx = P.idx; hp = P.hv;
                     }
-                    if (args.log) {
+                    if (args.log && leader) {
                         int r1, r2, a1, a2;
                         decode_move(s, E, pidx, r1, r2, a1, a2);
                         const Score sp = score_move(s, r1, r2, a1, a2);
@@ -751,13 +759,15 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 const bool nb = (ck1 < bk1) || (ck1 == bk1 && ck2 < bk2);
                 if (nb) {
                     bk1 = ck1; bk2 = ck2; best_step = k; best_idx = cidx; stall = 0;
-                    int c1, c2, c3, c4;
-                    decode_move(s, E, cidx, c1, c2, c3, c4);
-                    for (int e = 0; e < E; ++e) s.bw[e] = s.w[e];
-                    if (c1 != 0xFF) s.bw[c1] -= 1;
-                    if (c2 != 0xFF) s.bw[c2] -= 1;
-                    if (c3 != 0xFF) s.bw[c3] += 1;
-                    if (c4 != 0xFF) s.bw[c4] += 1;
+                    if (leader) {
+                        int c1, c2, c3, c4;
+                        decode_move(s, E, cidx, c1, c2, c3, c4);
+                        for (int e = 0; e < E; ++e) s.bw[e] = s.w[e];
+                        if (c1 != 0xFF) s.bw[c1] -= 1;
+                        if (c2 != 0xFF) s.bw[c2] -= 1;
+                        if (c3 != 0xFF) s.bw[c3] += 1;
+                        if (c4 != 0xFF) s.bw[c4] += 1;
+                    }
                 } else {
                     stall += 1;
                 }
@@ -765,7 +775,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 const double Tk = args.t_floor >= T0 ? args.t_floor : T0;
                 const double u = uniform01(derive_seed4(args.seed, gchain, (uint64_t)k, 0ULL));
                 const bool acc = (hp <= hc) || (u < exp_clv(-(hp - hc) / Tk));
-                if (args.log) {
+                if (args.log && leader) {
                     clv_log_row row;
                     row.temp = Tk; row.f = fp; row.h = hp; row.p95_ms = Lp;
                     row.iter = k; row.ged_from_center = (pidx < (long long)E * E) ? 2 : 4; row.sla_met = slap;
@@ -777,23 +787,11 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (stall >= args.stall_limit) { status = 1; fin = 1; }
             }
             if (!fin && k + 1 >= args.max_steps) { status = 0; fin = 1; }
-            s.dec_move = mv;
+            if (mv != NOIDX) apply_move(s, E, mv);
             s.dec_done = fin;
         }
         PROF_MARK(5);
-        cluster.sync();
         PROF_MARK(6);
-        if (tid == 0) {
-            long long mv;
-            int dn;
-            if (crank == 0) { mv = s.dec_move; dn = s.dec_done; }
-            else {
-                mv = *cluster.map_shared_rank(&s.dec_move, 0);
-                dn = *cluster.map_shared_rank(&s.dec_done, 0);
-                s.dec_move = mv; s.dec_done = dn;
-            }
-            if (mv != NOIDX) apply_move(s, E, mv);
-        }
         __syncthreads();
         done = s.dec_done;
         PROF_MARK(7);
