@@ -18,5 +18,4 @@ for cl in (3,):
     names=["prepare","score","cta_reduce","sync1","leader","sync2","apply"]
     lead=buf[:,0,:7].mean(0)/64; other=buf[:,1,:7].mean(0)/64
     print("cluster",cl,"cycles/step leader:", {k:int(v) for k,v in zip(names,lead)}, "\n  rank1:", {k:int(v) for k,v in zip(names,other)})
-    ev=b.host()['results']['evals'].sum()
-    print("screen survivors %d of %d candidates (%.3f)"%(buf[:,:,7].sum(), ev, buf[:,:,7].sum()/ev))
+

@@ -1,6 +1,5 @@
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
 CLV_ANNEAL_VARIANT=9 python tmp_prof.py
-for v in 0 3; do
+for v in 0 1 2 3; do
   echo "variant $v"; CLV_ANNEAL_VARIANT=$v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'])"
 done
-bash tools/sanitize.sh 2>&1 | grep -E "==|SUMMARY"
