@@ -151,6 +151,17 @@ def fp64_peak_tflops():
         return None, "unavailable: %s" % exc
 
 
+def _profile_evidence():
+    """DRAM traffic and issue-slot utilisation of the chain kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "anneal_traffic.json")) as fh:
+            d = json.load(fh)
+        return {"traffic": d["dram_bytes_read"] + d["dram_bytes_write"], "issue_active_pct": d["issue_active_pct"],
+                "source": d["source"]}
+    except (OSError, KeyError, ValueError):
+        return {}
+
+
 # ------------------------------------------------------------------- CPU legs
 def _cpu_chain(args):
     (w0, chain, seed, max_steps) = args
@@ -379,8 +390,13 @@ def main():
     per_launch_cand = evals / args.steps
     avg_anneal_s = sum(anneal_ms) / 1000.0 / args.steps
     achieved_tflops = per_launch_cand * FLOPS_PER_CANDIDATE / avg_anneal_s / 1e12
+    prof_ev = _profile_evidence()
     roof = {"bound": "fp64", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
-            "frac": (achieved_tflops / peak) if peak else None, "traffic": None,
+            "frac": (achieved_tflops / peak) if peak else None,
+            "traffic": prof_ev.get("traffic"),
+            "traffic_unit": "bytes per launch (dram read + write, ncu --set full)",
+            "issue_active_pct_ncu": prof_ev.get("issue_active_pct"),
+            "evidence": prof_ev.get("source"),
             "kernel": "clv::anneal_kernel", "peak_source": peak_src,
             "algorithmic": "%d fp64 ops per scored candidate (epilogue) x %.0f candidates per launch"
                            % (FLOPS_PER_CANDIDATE, per_launch_cand),

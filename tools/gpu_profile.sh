@@ -1,5 +1,6 @@
 #!/bin/bash
-# Run on the GPU box: bench line, launch list and one full ncu capture of the chain kernel.
+# Run on the GPU box: bench line, launch list, one full ncu capture of the chain kernel
+# and the per-phase cycle profile.  Outputs land in gpurun_out/ (summarise into profiles/).
 set -x
 mkdir -p gpurun_out
 python -m paper_2304_09781_b200.build
@@ -10,4 +11,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_run.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:anneal -s 2 -c 1 \
     -o gpurun_out/prof_anneal -f python bench.py --steps 1 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_run.log 2>&1
+CLV_ANNEAL_VARIANT=9 timeout 300 python tools/phase_profile.py > gpurun_out/phase_profile.txt 2>&1
 ls -la gpurun_out

@@ -1,4 +1,5 @@
-import sys; sys.path.insert(0,'.')
+"""Per-phase cycle profile of the chain kernel (CLV_ANNEAL_VARIANT=9 build variant): cycles per step by phase."""
+import sys; sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import numpy as np, torch, time, ctypes, os
 from paper_2304_09781_b200.engine import CloverEngine
 from paper_2304_09781_b200.profiles import synthetic_profile
