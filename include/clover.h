@@ -26,6 +26,9 @@
  *   clv_select_chains /
  *   clv_reduce_records      best tracking / fixed-order winner
  *   clv_derive_seed         derive_seed                               core.py:107-118
+ *   clv_set_sim_profile /
+ *   clv_simulate            simulate / p95 / overall_accuracy (batched serving DES,
+ *                           one independent simulation per candidate)
  */
 #ifndef CLOVER_B200_H
 #define CLOVER_B200_H
@@ -130,6 +133,26 @@ typedef struct clv_pod {
     clv_eval_params params;
 } clv_pod;
 
+/* Serving workload of the discrete-event simulator. */
+typedef struct clv_workload {
+    double arrival_rps;      /* Poisson rate (or 1 / period in periodic mode)     */
+    double duration_s;       /* arrivals in [0, duration)                          */
+    uint64_t seed;           /* counter-RNG key of arrivals and service draws      */
+    int32_t periodic;        /* 1 = the SPEC's degenerate periodic-arrival mode    */
+    int32_t warmup;          /* completions excluded from latency stats; -1 = max(100, N/20) */
+} clv_workload;
+
+/* One simulation's SimReport. */
+typedef struct clv_sim_report {
+    double p95_ms, mean_latency_ms, throughput_rps;
+    double energy_wh_total, energy_wh_per_request;   /* per request = active energy / completed */
+    double accuracy;                                 /* overall_accuracy */
+    int64_t completed;       /* requests served (all arrivals)                     */
+    int64_t counted;         /* requests in the latency statistics (after warm-up) */
+    int32_t sla_met;         /* p95_ms <= l_tail_ms                                */
+    int32_t status;          /* 0 ok, else a clv_status of this simulation          */
+} clv_sim_report;
+
 int clv_abi_version(void);
 int clv_create(int device, clv_ctx **out);
 void clv_destroy(clv_ctx *ctx);
@@ -179,6 +202,22 @@ int clv_sweep(clv_ctx *ctx, int n_pods, const clv_pod *pods, int64_t begin, int6
 int clv_sweep_decode(clv_ctx *ctx, int n_pods, const clv_pod *pods, uint64_t seed,
                      int64_t index, int32_t *partitions_host, int32_t *assignments_host,
                      int32_t *n_assignments);
+
+/* Simulator rows of a profile family: per edge e = (v-1)*5 + slice index the mean
+ * service time, distribution (0 deterministic, 1 exponential, 2 lognormal), sigma
+ * and active energy per request; idle power per slice kind; accuracy per variant. */
+int clv_set_sim_profile(clv_ctx *ctx, int family, int n_variants, const double *mean_service_ms,
+                        const int32_t *dist, const double *sigma, const double *energy_wh,
+                        const double *idle_w5, const double *accuracy, const uint8_t *mem_ok);
+/* Simulate `count` fleets.  Fleet c's instances are inst_edge_dev[inst_off_dev[c] ..
+ * inst_off_dev[c+1]) (edge ids in FleetConfig.instances() order, at most
+ * max_instances).  reports_dev[count]; optional variant_counts_dev[count][8] and
+ * instance_counts_dev[inst_off[count]].  *n_requests (host, optional) receives the
+ * workload's request count.  Synchronises the stream once (request-count readback). */
+int clv_simulate(clv_ctx *ctx, int family, const clv_workload *workload, int64_t count,
+                 const uint8_t *inst_edge_dev, const int64_t *inst_off_dev, int max_instances,
+                 double l_tail_ms, clv_sim_report *reports_dev, int64_t *variant_counts_dev,
+                 int64_t *instance_counts_dev, int64_t *n_requests, void *stream);
 
 #ifdef __cplusplus
 }

@@ -56,6 +56,17 @@ class Pod(ctypes.Structure):
     _fields_ = [("family", c_i32), ("n_gpus", c_i32), ("weight", c_f64), ("params", EvalParams)]
 
 
+class Workload(ctypes.Structure):
+    _fields_ = [("arrival_rps", c_f64), ("duration_s", c_f64), ("seed", c_u64), ("periodic", c_i32),
+                ("warmup", c_i32)]
+
+
+class SimReport(ctypes.Structure):
+    _fields_ = [("p95_ms", c_f64), ("mean_latency_ms", c_f64), ("throughput_rps", c_f64),
+                ("energy_wh_total", c_f64), ("energy_wh_per_request", c_f64), ("accuracy", c_f64),
+                ("completed", c_i64), ("counted", c_i64), ("sla_met", c_i32), ("status", c_i32)]
+
+
 STATUS_TO_ERROR = {
     1: E.CarbonSchedError, 2: E.InvalidConfigError, 3: E.InfeasibleAssignmentError,
     4: E.IncompatibleGraphsError, 5: E.InfeasibleGraphError, 6: E.NoNeighborError,
@@ -90,6 +101,9 @@ SIGNATURES = {
     "clv_reduce_records": (c_i32, [c_vp, c_vp, c_i32, c_vp, c_vp]),
     "clv_sweep": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_i64, c_u64, c_vp, c_vp, c_vp, ctypes.POINTER(Best), c_vp]),
     "clv_sweep_decode": (c_i32, [c_vp, c_i32, c_vp, c_u64, c_i64, c_vp, c_vp, ctypes.POINTER(c_i32)]),
+    "clv_set_sim_profile": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "clv_simulate": (c_i32, [c_vp, c_i32, ctypes.POINTER(Workload), c_i64, c_vp, c_vp, c_i32, c_f64, c_vp, c_vp,
+                             c_vp, ctypes.POINTER(c_i64), c_vp]),
 }
 
 _lib = None

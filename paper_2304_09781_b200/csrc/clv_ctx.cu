@@ -6,44 +6,10 @@
 #include <cstring>
 #include <string>
 #include <vector>
-#include "clv_internal.h"
+#include "clv_ctx.h"
 
 using namespace clv;
 
-struct clv_ctx {
-    int device = 0;
-    int sm_count = 148;
-    std::string err;
-    bool topo_set = false;
-    Topology topo{};
-    double mem_gb[CLV_K] = {0, 0, 0, 0, 0};
-    Topology *topo_dev = nullptr;
-    bool fam_set[CLV_MAX_FAMILIES] = {};
-    FamilyTables fam[CLV_MAX_FAMILIES];
-    uint32_t *pair_list_dev[CLV_MAX_FAMILIES] = {};
-    FamilyTables *fam_dev = nullptr;
-    // feasibility tables
-    int feas_nmax = -1;
-    int bdim = 0, cdim = 0;
-    uint32_t *feas_bits = nullptr;
-    uint32_t *feas_off = nullptr;
-    size_t feas_words = 0;
-    // selection scratch
-    int max_blocks = 0;
-    RecP *partials = nullptr;
-    unsigned long long *pcnt = nullptr;
-    unsigned int *done_counter = nullptr;
-    RecP *final_rec = nullptr;
-    unsigned long long *final_cnt = nullptr;
-    RecP *host_rec = nullptr;                 // pinned
-    unsigned long long *host_cnt = nullptr;   // pinned
-    int *err_flag = nullptr;
-    long long *err_index = nullptr;
-    int *host_err = nullptr;                  // pinned [2 ints + 1 ll]
-    EvalConst *ec_dev = nullptr;
-    int ec_cap = 0;
-    int32_t *small_dev = nullptr;             // realize scratch
-};
 
 namespace {
 
@@ -204,6 +170,7 @@ void clv_destroy(clv_ctx *ctx) {
     cudaFree(ctx->err_flag); cudaFree(ctx->err_index); cudaFreeHost(ctx->host_err);
     cudaFree(ctx->ec_dev); cudaFree(ctx->small_dev);
     for (int f = 0; f < CLV_MAX_FAMILIES; ++f) cudaFree(ctx->pair_list_dev[f]);
+    clv::sim_destroy(ctx->sim);
     delete ctx;
 }
 

@@ -141,8 +141,32 @@ class CloverEngine:
         self._check(self.lib.clv_set_profile(self.ctx, fam, t.variant_count, thr.ctypes.data, acc.ctypes.data,
                                              en.ctypes.data, idle.ctypes.data, lat.ctypes.data, mem.ctypes.data,
                                              t.kt, t.ke, t.ki))
+        self._set_sim_profile(fam, profile)
         self._families[profile.name] = (fam, profile, t)
         return fam
+
+    def _set_sim_profile(self, fam: int, profile: ProfileTable) -> None:
+        """Simulator rows of the family: per edge mean, distribution, sigma, energy."""
+        from .profiles import DISTS
+        V = profile.variant_count
+        E = 5 * V
+        mean = np.zeros(E, dtype=np.float64)
+        dist = np.zeros(E, dtype=np.int32)
+        sigma = np.zeros(E, dtype=np.float64)
+        energy = np.zeros(E, dtype=np.float64)
+        mem = np.zeros(E, dtype=np.uint8)
+        for v in range(1, V + 1):
+            for s in SLICE_ORDER:
+                e = (v - 1) * 5 + s.index
+                row = profile.service[(v, s)]
+                mean[e], dist[e], sigma[e] = row.mean_service_ms, DISTS.index(row.dist), row.sigma
+                energy[e] = row.energy_wh_per_request
+                mem[e] = 1 if profile.memory_feasible(v, s) else 0
+        idle = np.array([profile.idle_power_w[s] for s in SLICE_ORDER], dtype=np.float64)
+        acc = np.array([profile.accuracy(v) for v in range(1, V + 1)], dtype=np.float64)
+        self._check(self.lib.clv_set_sim_profile(self.ctx, fam, V, mean.ctypes.data, dist.ctypes.data,
+                                                 sigma.ctypes.data, energy.ctypes.data, idle.ctypes.data,
+                                                 acc.ctypes.data, mem.ctypes.data))
 
     def family(self, profile: ProfileTable) -> int:
         return self.add_profile(profile)
@@ -387,3 +411,49 @@ class CloverEngine:
             g0 += n_gpus
             s0 += m
         return out
+
+    # -- serving simulator ---------------------------------------------
+    def simulate(self, inst_edges, offsets, profile: ProfileTable, workload, l_tail_ms: float = float("inf"),
+                 counts: bool = True, stream=None):
+        """One discrete-event simulation per fleet (clv_simulate).
+
+        inst_edges: uint8 edge id per instance, fleets concatenated (FleetConfig.instances()
+        order); offsets: int64 [count + 1].  Host arrays are copied to the device; device
+        tensors are used in place.  Returns (reports (SIM_DTYPE), variant_counts [count, 8] or
+        None, instance_counts [total] or None, n_requests)."""
+        torch = self.torch
+        fam = self.add_profile(profile)
+        dev = "cuda:%d" % self.device
+        if not isinstance(inst_edges, torch.Tensor):
+            inst_edges = torch.from_numpy(np.ascontiguousarray(inst_edges, dtype=np.uint8)).to(dev)
+        if not isinstance(offsets, torch.Tensor):
+            off_h = np.ascontiguousarray(offsets, dtype=np.int64)
+            kmax = int(np.max(np.diff(off_h))) if len(off_h) > 1 else 1
+            offsets = torch.from_numpy(off_h).to(dev)
+        else:
+            kmax = int(torch.diff(offsets).max().item()) if offsets.numel() > 1 else 1
+        count = int(offsets.numel()) - 1
+        total = int(inst_edges.numel())
+        rep = torch.empty(max(count, 1) * SIM_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        vc = torch.zeros((max(count, 1), 8), dtype=torch.int64, device=dev) if counts else None
+        ic = torch.zeros(max(total, 1), dtype=torch.int64, device=dev) if counts else None
+        w = workload_c(workload)
+        nreq = ctypes.c_int64(0)
+        self._check(self.lib.clv_simulate(self.ctx, fam, ctypes.byref(w), count, inst_edges.data_ptr(),
+                                          offsets.data_ptr(), max(1, kmax), float(l_tail_ms), rep.data_ptr(),
+                                          _ptr(vc), _ptr(ic), ctypes.byref(nreq), self._stream(stream)))
+        reps = np.frombuffer(rep.cpu().numpy().tobytes(), dtype=SIM_DTYPE)[:count]
+        return (reps, None if vc is None else vc.cpu().numpy()[:count],
+                None if ic is None else ic.cpu().numpy()[:total], int(nreq.value))
+
+
+SIM_DTYPE = np.dtype([("p95_ms", "<f8"), ("mean_latency_ms", "<f8"), ("throughput_rps", "<f8"),
+                      ("energy_wh_total", "<f8"), ("energy_wh_per_request", "<f8"), ("accuracy", "<f8"),
+                      ("completed", "<i8"), ("counted", "<i8"), ("sla_met", "<i4"), ("status", "<i4")])
+assert SIM_DTYPE.itemsize == ctypes.sizeof(N.SimReport) == 72
+
+
+def workload_c(w) -> N.Workload:
+    warm = -1 if w.warmup is None else int(w.warmup)
+    return N.Workload(float(w.arrival_rate_rps), float(w.duration_s), int(w.seed) & ((1 << 64) - 1),
+                      1 if w.periodic else 0, warm)

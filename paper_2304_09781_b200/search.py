@@ -23,6 +23,7 @@ from .graph import ConfigGraph, build_graph
 from .mig import FleetConfig
 from .objective import AnnealParams, Scenario, strict_eq6_default
 from .profiles import ProfileTable
+from .sim import Workload  # noqa: F401  (re-exported)
 
 _ENGINES: dict = {}
 
@@ -36,15 +37,6 @@ def default_engine(topology=None) -> CloverEngine:
     if key not in _ENGINES:
         _ENGINES[key] = CloverEngine(topo)
     return _ENGINES[key]
-
-
-@dataclass(frozen=True)
-class Workload:
-    """Poisson request stream; the surrogate uses the rate only."""
-
-    arrival_rate_rps: float
-    duration_s: float = 600.0
-    seed: int = 0
 
 
 @dataclass
