@@ -16,11 +16,12 @@
 //     exact prefix sums of rounded exponential gaps), and per-request draws
 //     ex[N] (unit exponential) and z[N] (standard normal), shared by every fleet;
 //   * sim_kernel: one WARP per simulation for the sequential queue recursion.
-//     Instance free times live in the warp's shared-memory slab; lane l owns
-//     instances j = l (mod 32) and caches its own (min free, index); each request
-//     is one 3-step redux.sync argmin over the lanes, the owner lane serves it and
-//     rescans its slots.  Completions go to a per-warp HBM scratch row c[N]
-//     (coalesced 32-request stores).  Then the whole CTA post-processes its
+//     Instance keys (free << 11 | j) live in the warp's shared-memory slab, lane g
+//     caches the minimum of instance group g = {g, g+32, ...}; each request is a
+//     2-step redux.sync argmin over the group minima, a warp-uniform service draw,
+//     and a 2-step redux.sync refresh of the served instance's group.
+//     Completions go to a per-warp HBM scratch row c[N] (coalesced 32-request
+//     stores).  Then the whole CTA post-processes its
 //     simulations one at a time: 11-bit radix selections for the warm-up cut (key
 //     = completion << b | request) and the nearest-rank p95 over the remaining
 //     latencies, exact integer sums for mean latency / busy / idle time, and the
@@ -44,7 +45,12 @@ struct SimFamily {
     double energy_wh[CLV_MAX_EDGES];
     double idle_w[CLV_K];
     double acc[CLV_MAX_VARIANTS];
+    int cls[CLV_MAX_EDGES];                  // service class of the edge
+    int n_cls;
+    int cls_kind[8];                         // 0 deterministic, 1 exponential, 2 lognormal
+    double cls_sigma[8], cls_hs[8];
 };
+constexpr int SIM_MAX_CLS = 8;
 
 struct SimState {
     bool fam_set[CLV_MAX_FAMILIES] = {};
@@ -62,7 +68,10 @@ struct SimState {
     long long *n_host = nullptr;             // pinned
     // completion scratch: slots x N int64
     long long *c_scr = nullptr;
+    unsigned short *j_scr = nullptr;
     size_t scr_elems = 0;
+    double *mult = nullptr;                  // [n_cls][N] service multipliers
+    size_t mult_elems = 0;
 };
 
 void sim_destroy(SimState *s) {
@@ -70,7 +79,7 @@ void sim_destroy(SimState *s) {
     cudaFree(s->fam_dev);
     cudaFree(s->a); cudaFree(s->ex); cudaFree(s->z); cudaFree(s->n_dev);
     cudaFreeHost(s->n_host);
-    cudaFree(s->c_scr);
+    cudaFree(s->c_scr); cudaFree(s->j_scr); cudaFree(s->mult);
     delete s;
 }
 
@@ -159,7 +168,9 @@ struct SimArgs {
     const uint8_t *inst_edge;
     const int64_t *inst_off;
     int kmax, key_bits;
+    const double *mult;
     long long *c_scr;
+    unsigned short *j_scr;
     clv_sim_report *rep;
     int64_t *vcnt;
     int64_t *icnt;
@@ -265,6 +276,42 @@ __device__ unsigned long long radix_select(long long N, long long k, int nbits, 
     return prefix;
 }
 
+// Per-request service multipliers of the family's service classes (class 0:
+// deterministic = 1, 1: exponential = ex_i, k >= 2: lognormal exp(sigma_k z_i - hs_k)).
+__global__ void sim_mult_kernel(const SimFamily *fam, const double *ex, const double *z, long long N, double *mult) {
+    const SimFamily &F = *fam;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+        for (int k = 0; k < F.n_cls; ++k) {
+            double m = 1.0;
+            if (F.cls_kind[k] == 1) m = ex[i];
+            else if (F.cls_kind[k] == 2) m = exp_clv(F.cls_sigma[k] * z[i] - F.cls_hs[k]);
+            mult[(size_t)k * N + i] = m;
+        }
+    }
+}
+
+// Per-warp shared-memory slab of one simulation (kmax instances).
+struct Slab {
+    unsigned long long *key;   // (free << 11) | j during the run; busy time (ns) in the post-pass
+    long long *svc;            // deterministic service ns (RAND=false) / mean ns as double bits (RAND=true)
+    unsigned *cnt;
+    unsigned char *ed, *cls;
+    double *mst;               // [SIM_MAX_CLS][32] multipliers of the current 32-request block
+};
+__device__ __forceinline__ Slab slab_of(unsigned char *base, int kmax) {
+    Slab q;
+    q.mst = reinterpret_cast<double *>(base);
+    q.key = reinterpret_cast<unsigned long long *>(base + SIM_MAX_CLS * 32 * 8);
+    q.svc = reinterpret_cast<long long *>(q.key + kmax);
+    q.cnt = reinterpret_cast<unsigned *>(q.svc + kmax);
+    q.ed = reinterpret_cast<unsigned char *>(q.cnt + kmax);
+    q.cls = q.ed + kmax;
+    return q;
+}
+__host__ __device__ inline size_t slab_bytes(int kmax) {
+    return ((size_t)SIM_MAX_CLS * 32 * 8 + (size_t)kmax * 22 + 15) & ~(size_t)15;
+}
+
 template <bool RAND>
 __global__ void __launch_bounds__(SNT) sim_kernel(const __grid_constant__ SimArgs args) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -282,20 +329,17 @@ __global__ void __launch_bounds__(SNT) sim_kernel(const __grid_constant__ SimArg
         int *dst = reinterpret_cast<int *>(&F);
         for (int q = tid; q < (int)(sizeof(SimFamily) / 4); q += SNT) dst[q] = src[q];
     }
-    // per-warp slab: free[kmax] int64 | busy[kmax] int64 | cnt[kmax] u32 | edge[kmax] u8
-    const size_t slab = (size_t)kmax * 21 + 16;
-    const size_t slab_al = (slab + 15) & ~(size_t)15;
+    const size_t sb = slab_bytes(kmax);
     const long long N = args.N;
     __syncthreads();
+    const int C = F.n_cls;
 
     for (long long base = (long long)blockIdx.x * SNW; base < args.count; base += (long long)gridDim.x * SNW) {
         const long long sim = base + warp;
-        unsigned char *my = smem_raw + slab_al * warp;
-        long long *fr = reinterpret_cast<long long *>(my);
-        long long *bs = fr + kmax;
-        unsigned *cn = reinterpret_cast<unsigned *>(bs + kmax);
-        unsigned char *ed = reinterpret_cast<unsigned char *>(cn + kmax);
-        long long *cs = args.c_scr + ((long long)blockIdx.x * SNW + warp) * N;
+        const Slab q = slab_of(smem_raw + sb * warp, kmax);
+        const size_t row = ((size_t)blockIdx.x * SNW + warp) * (size_t)N;
+        long long *cs = args.c_scr + row;
+        unsigned short *js = args.j_scr + row;
         int status = 0, K = 0;
         if (sim < args.count) {
             const long long o0 = args.inst_off[sim], o1 = args.inst_off[sim + 1];
@@ -305,10 +349,14 @@ __global__ void __launch_bounds__(SNT) sim_kernel(const __grid_constant__ SimArg
             } else {
                 int bad = 0;
                 for (int t = lane; t < K; t += 32) {
-                    const int e = args.inst_edge[o0 + t];
-                    if (e >= F.E) bad |= 2;
+                    int e = args.inst_edge[o0 + t];
+                    if (e >= F.E) { bad |= 2; e = 0; }
                     else if (!((F.mem_ok >> e) & 1ULL)) bad |= 1;
-                    ed[t] = (unsigned char)e; fr[t] = 0; bs[t] = 0; cn[t] = 0u;
+                    q.ed[t] = (unsigned char)e;
+                    q.cls[t] = (unsigned char)F.cls[e];
+                    q.svc[t] = RAND ? __double_as_longlong(F.mean_ns[e]) : F.det_ns[e];
+                    q.key[t] = (unsigned long long)t;
+                    q.cnt[t] = 0u;
                 }
                 bad = __reduce_or_sync(0xFFFFFFFFu, bad);
                 if (bad & 2) status = CLV_ERR_SIMULATION;
@@ -316,48 +364,49 @@ __global__ void __launch_bounds__(SNT) sim_kernel(const __grid_constant__ SimArg
             }
             __syncwarp();
             if (status == 0) {
-                long long lmin = lane < K ? 0LL : LLONG_MAX;
-                unsigned lidx = lane < K ? (unsigned)lane : 0xFFFFFFFFu;
+                // Slot j holds the packed key (free_j << 11) | j (unique, order-preserving: the
+                // argmin key is argmin (free, j)); lane g caches the minimum of instance group
+                // g = {g, g+32, ...}; slot j is read and written only by lane j >> 5.
+                unsigned long long gm = lane < K ? (unsigned long long)lane : ~0ULL;
                 for (long long b = 0; b < N; b += 32) {
                     const long long i = b + lane;
-                    long long al = 0;
-                    double exl = 0.0, zl = 0.0;
-                    if (i < N) {
-                        al = __ldg(args.a + i);
-                        if (RAND) { exl = __ldg(args.ex + i); zl = __ldg(args.z + i); }
+                    const long long al = i < N ? __ldg(args.a + i) : 0LL;
+                    if (RAND) {
+                        __syncwarp();
+                        for (int k = 0; k < C; ++k)
+                            q.mst[k * 32 + lane] = i < N ? __ldg(args.mult + (size_t)k * N + i) : 1.0;
+                        __syncwarp();
                     }
                     const int nb = (int)min(32LL, N - b);
                     long long myc = 0;
+                    unsigned myj = 0;
+#pragma unroll 4
                     for (int r = 0; r < nb; ++r) {
                         const long long ai = __shfl_sync(0xFFFFFFFFu, al, r);
-                        const unsigned hi = (unsigned)((unsigned long long)lmin >> 32), lo = (unsigned)lmin;
+                        const unsigned hi = (unsigned)(gm >> 32);
                         const unsigned mh = __reduce_min_sync(0xFFFFFFFFu, hi);
-                        const unsigned ml = __reduce_min_sync(0xFFFFFFFFu, hi == mh ? lo : 0xFFFFFFFFu);
-                        const unsigned mj = __reduce_min_sync(0xFFFFFFFFu, (hi == mh && lo == ml) ? lidx : 0xFFFFFFFFu);
-                        const long long fv = (long long)(((unsigned long long)mh << 32) | ml);
-                        const long long start = ai > fv ? ai : fv;
-                        double exi = 0.0, zi = 0.0;
-                        if (RAND) { exi = __shfl_sync(0xFFFFFFFFu, exl, r); zi = __shfl_sync(0xFFFFFFFFu, zl, r); }
-                        long long c = 0;
-                        const int owner = (int)(mj & 31u);
-                        if (lane == owner) {
-                            const long long s = service_ns(F, ed[mj], exi, zi);
-                            c = start + s;
-                            fr[mj] = c;
-                            bs[mj] += s;
-                            cn[mj] += 1u;
-                            long long m = LLONG_MAX;
-                            unsigned mi = 0xFFFFFFFFu;
-                            for (int t = lane; t < K; t += 32) {
-                                const long long v = fr[t];
-                                if (v < m) { m = v; mi = (unsigned)t; }
-                            }
-                            lmin = m; lidx = mi;
-                        }
-                        c = __shfl_sync(0xFFFFFFFFu, c, owner);
-                        if (lane == r) myc = c;
+                        const unsigned ml = __reduce_min_sync(0xFFFFFFFFu, hi == mh ? (unsigned)gm : 0xFFFFFFFFu);
+                        const unsigned long long P = ((unsigned long long)mh << 32) | ml;
+                        const int j = (int)(ml & 2047u);
+                        const long long fv = (long long)(P >> 11);
+                        // the rest of j's group (independent of the service draw)
+                        const int g = j & 31;
+                        const int slot = g + 32 * lane;
+                        const unsigned long long vo = (slot < K && slot != j) ? q.key[slot] : ~0ULL;
+                        long long sv;
+                        if (RAND) sv = round_ns(__longlong_as_double(q.svc[j]) * q.mst[q.cls[j] * 32 + r]);
+                        else sv = q.svc[j];
+                        const long long c = (ai > fv ? ai : fv) + sv;
+                        const unsigned long long np = ((unsigned long long)c << 11) | (unsigned)j;
+                        const unsigned h2 = (unsigned)(vo >> 32);
+                        const unsigned m2 = __reduce_min_sync(0xFFFFFFFFu, h2);
+                        const unsigned l2 = __reduce_min_sync(0xFFFFFFFFu, h2 == m2 ? (unsigned)vo : 0xFFFFFFFFu);
+                        const unsigned long long mo = ((unsigned long long)m2 << 32) | l2;
+                        if (lane == g) gm = mo < np ? mo : np;
+                        if (lane == (j >> 5)) q.key[j] = np;
+                        if (lane == r) { myc = c; myj = (unsigned)j; }
                     }
-                    if (i < N) cs[i] = myc;
+                    if (i < N) { cs[i] = myc; js[i] = (unsigned short)myj; }
                 }
             }
         }
@@ -370,16 +419,26 @@ __global__ void __launch_bounds__(SNT) sim_kernel(const __grid_constant__ SimArg
             if (sw >= args.count) break;
             int st = s_status[w];
             const int Kw = s_K[w];
-            const long long *cw = args.c_scr + ((long long)blockIdx.x * SNW + w) * N;
-            unsigned char *mw = smem_raw + slab_al * w;
-            const long long *bw = reinterpret_cast<const long long *>(mw) + kmax;
-            const unsigned *nw = reinterpret_cast<const unsigned *>(bw + kmax);
-            const unsigned char *ew = reinterpret_cast<const unsigned char *>(nw + kmax);
+            const size_t roww = ((size_t)blockIdx.x * SNW + w) * (size_t)N;
+            const long long *cw = args.c_scr + roww;
+            const unsigned short *jw = args.j_scr + roww;
+            const Slab qw = slab_of(smem_raw + sb * w, kmax);
             clv_sim_report rp;
             memset(&rp, 0, sizeof(rp));
             if (st == 0) {
+                for (int t = tid; t < Kw; t += SNT) qw.key[t] = 0ULL;     // busy time
+                __syncthreads();
                 long long mx = 0;
-                for (long long i = tid; i < N; i += SNT) mx = max(mx, cw[i]);
+                for (long long i = tid; i < N; i += SNT) {
+                    const long long c = cw[i];
+                    const int j = jw[i];
+                    long long sv;
+                    if (RAND) sv = round_ns(__longlong_as_double(qw.svc[j]) * __ldg(args.mult + (size_t)qw.cls[j] * N + i));
+                    else sv = qw.svc[j];
+                    atomicAdd(&qw.cnt[j], 1u);
+                    atomicAdd(&qw.key[j], (unsigned long long)sv);
+                    mx = max(mx, c);
+                }
                 const long long t_end = max(args.d_ns, block_max(mx, lbuf));
                 const int b = args.key_bits;
                 if (t_end >= (1LL << (63 - b))) st = CLV_ERR_SIMULATION;   // completion key would overflow
@@ -403,14 +462,14 @@ __global__ void __launch_bounds__(SNT) sim_kernel(const __grid_constant__ SimArg
                         if (counted(i)) ls += (unsigned long long)(cw[i] - __ldg(args.a + i));
                     const unsigned long long lsum = block_sum(ls, wbuf);
                     // per-instance aggregation (exact integers)
-                    for (int q = tid; q < CLV_MAX_EDGES; q += SNT) cnt_e[q] = 0ULL;
+                    for (int e = tid; e < CLV_MAX_EDGES; e += SNT) cnt_e[e] = 0ULL;
                     if (tid < CLV_K) idle_s[tid] = 0ULL;
                     __syncthreads();
                     for (int t = tid; t < Kw; t += SNT) {
-                        const int e = ew[t];
-                        atomicAdd(&cnt_e[e], (unsigned long long)nw[t]);
-                        atomicAdd(&idle_s[e % CLV_K], (unsigned long long)(t_end - bw[t]));
-                        if (args.icnt) args.icnt[args.inst_off[sw] + t] = (int64_t)nw[t];
+                        const int e = qw.ed[t];
+                        atomicAdd(&cnt_e[e], (unsigned long long)qw.cnt[t]);
+                        atomicAdd(&idle_s[e % CLV_K], (unsigned long long)(t_end - (long long)qw.key[t]));
+                        if (args.icnt) args.icnt[args.inst_off[sw] + t] = (int64_t)qw.cnt[t];
                     }
                     __syncthreads();
                     if (tid == 0) {
@@ -561,6 +620,20 @@ int clv_set_sim_profile(clv_ctx *ctx, int family, int V, const double *mean_ms, 
         if (dist[e] != 0) T.any_random = 1;
         if (mem_ok[e]) T.mem_ok |= 1ULL << e;
     }
+    // service classes: 0 deterministic, 1 exponential, then one per distinct lognormal sigma
+    T.n_cls = 2;
+    T.cls_kind[0] = 0; T.cls_kind[1] = 1;
+    for (int e = 0; e < T.E; ++e) {
+        if (T.dist[e] < 2) { T.cls[e] = T.dist[e]; continue; }
+        int k = 2;
+        while (k < T.n_cls && T.cls_sigma[k] != T.sigma[e]) ++k;
+        if (k == T.n_cls) {
+            if (k >= SIM_MAX_CLS) return sfail(ctx, CLV_ERR_PROFILE, "at most 6 distinct lognormal sigmas per profile");
+            T.cls_kind[k] = 2; T.cls_sigma[k] = T.sigma[e]; T.cls_hs[k] = T.hs[e];
+            T.n_cls++;
+        }
+        T.cls[e] = k;
+    }
     for (int k = 0; k < CLV_K; ++k) {
         if (!(idle_w5[k] >= 0) || !std::isfinite(idle_w5[k])) return sfail(ctx, CLV_ERR_PROFILE, "idle power must be >= 0");
         T.idle_w[k] = idle_w5[k];
@@ -590,7 +663,7 @@ int clv_simulate(clv_ctx *ctx, int family, const clv_workload *w, int64_t count,
     if (w->warmup < -1) return sfail(ctx, CLV_ERR_SIMULATION, "warmup must be >= 0 or -1 (SPEC default)");
     if (std::isnan(l_tail_ms)) return sfail(ctx, CLV_ERR_SIMULATION, "l_tail is NaN");
     if (count < 0) return sfail(ctx, CLV_ERR_SIMULATION, "negative count");
-    if (max_instances < 1 || max_instances > 4096) return sfail(ctx, CLV_ERR_SIMULATION, "max_instances must be in 1..4096");
+    if (max_instances < 1 || max_instances > 2048) return sfail(ctx, CLV_ERR_SIMULATION, "max_instances must be in 1..2048");
     cudaStream_t st = (cudaStream_t)stream;
     SIM_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
     int rc = prepare_workload(ctx, S, *w, st);
@@ -603,37 +676,50 @@ int clv_simulate(clv_ctx *ctx, int family, const clv_workload *w, int64_t count,
     int key_bits = 1;
     while ((1LL << key_bits) < N) ++key_bits;
 
-    const size_t slab = (size_t)max_instances * 21 + 16;
-    const size_t slab_al = (slab + 15) & ~(size_t)15;
-    const size_t dyn = slab_al * SNW;
+    const size_t dyn = slab_bytes(max_instances) * SNW;
     const bool rnd = S->fam[family].any_random != 0;
+    if (rnd) {
+        const size_t m = (size_t)S->fam[family].n_cls * (size_t)N;
+        if (m > S->mult_elems) {
+            cudaFree(S->mult);
+            S->mult = nullptr; S->mult_elems = 0;
+            SIM_CUDA(cudaMalloc(&S->mult, m * sizeof(double)), "alloc multipliers");
+            S->mult_elems = m;
+        }
+        const int g = (int)std::min<long long>((N + 255) / 256, (long long)ctx->sm_count * 8);
+        sim_mult_kernel<<<std::max(g, 1), 256, 0, st>>>(S->fam_dev + family, S->ex, S->z, N, S->mult);
+        SIM_CUDA(cudaGetLastError(), "sim multipliers");
+    }
     auto kern = rnd ? sim_kernel<true> : sim_kernel<false>;
     SIM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn), "sim smem");
     int occ = 0;
     SIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SNT, dyn), "sim occupancy");
     if (occ < 1) return sfail(ctx, CLV_ERR_SIMULATION, "too many instances per fleet for shared memory");
     long long grid = std::min<long long>((count + SNW - 1) / SNW, (long long)occ * ctx->sm_count);
-    // completion scratch: grid x SNW rows of N int64, capped by a memory budget
+    // per-request scratch (completion int64 + instance uint16): grid x SNW rows of N, capped by a budget
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    size_t budget = std::min<size_t>((size_t)16 << 30, free_b / 2 + S->scr_elems * sizeof(long long));
+    const size_t per = sizeof(long long) + sizeof(unsigned short);
+    size_t budget = std::min<size_t>((size_t)16 << 30, free_b / 2 + S->scr_elems * per);
     const char *env = getenv("CLV_SIM_SCRATCH_MB");
     if (env) budget = (size_t)atoll(env) << 20;
-    const size_t row = (size_t)N * sizeof(long long) * SNW;
+    const size_t row = (size_t)N * per * SNW;
     grid = std::min<long long>(grid, (long long)(budget / std::max<size_t>(row, 1)));
     if (grid < 1) return sfail(ctx, CLV_ERR_OUT_OF_MEMORY, "simulation scratch does not fit the memory budget");
     const size_t need = (size_t)grid * SNW * (size_t)N;
     if (need > S->scr_elems) {
-        cudaFree(S->c_scr);
-        S->c_scr = nullptr; S->scr_elems = 0;
+        cudaFree(S->c_scr); cudaFree(S->j_scr);
+        S->c_scr = nullptr; S->j_scr = nullptr; S->scr_elems = 0;
         SIM_CUDA(cudaMalloc(&S->c_scr, need * sizeof(long long)), "alloc sim scratch");
+        SIM_CUDA(cudaMalloc(&S->j_scr, need * sizeof(unsigned short)), "alloc sim scratch");
         S->scr_elems = need;
     }
     SimArgs a{};
     a.fam = S->fam_dev + family; a.a = S->a; a.ex = S->ex; a.z = S->z;
     a.N = N; a.d_ns = S->d_ns; a.W = W; a.duration_s = w->duration_s;
     a.l_tail = l_tail_ms; a.count = count; a.inst_edge = inst_edge_dev; a.inst_off = inst_off_dev;
-    a.kmax = max_instances; a.key_bits = key_bits; a.c_scr = S->c_scr; a.rep = reports_dev;
+    a.kmax = max_instances; a.key_bits = key_bits; a.c_scr = S->c_scr; a.j_scr = S->j_scr; a.mult = S->mult;
+    a.rep = reports_dev;
     a.vcnt = variant_counts_dev; a.icnt = instance_counts_dev;
     kern<<<(unsigned)grid, SNT, dyn, st>>>(a);
     SIM_CUDA(cudaGetLastError(), "sim kernel");
