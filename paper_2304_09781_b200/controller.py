@@ -71,6 +71,8 @@ class TimelineReport:
     rows: list = field(default_factory=list)
     replans: list = field(default_factory=list)
     summary: dict = field(default_factory=dict)
+    evals_log: Optional[np.ndarray] = None     # LOG_DTYPE [1, max_steps] of the last Clover re-plan
+    evals_steps: Optional[list] = None
 
 
 def _score(engine, profile, w, scenario):
@@ -97,8 +99,17 @@ def _changed_gpus(a, b) -> int:
 def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, profile: ProfileTable,
               lam: float = 0.5, ap: Optional[AnnealParams] = None, cp: ControllerParams = ControllerParams(),
               seed: int = 0, chains: int = 128, utilization: float = 0.7, strict_sla: bool = True,
-              pue: float = 1.5, chain_base: int = 0, group=None) -> TimelineReport:
-    """Trace-driven control loop for ``scheme`` in SCHEMES."""
+              pue: float = 1.5, chain_base: int = 0, group=None, des_window_s: float = 0.0,
+              des_top: int = 16, log_evals: bool = False) -> TimelineReport:
+    """Trace-driven control loop for ``scheme`` in SCHEMES.
+
+    ``des_window_s`` > 0 turns on DES confirmation: L_tail_DES is the
+    simulated p95 of BASE (sla_from_base); at every Clover re-plan the
+    ``des_top`` best distinct chain winners (surrogate order: SLA first, then h) are
+    realized and simulated in one batch, and the first whose simulated p95 meets
+    L_tail_DES is the candidate; every timeline row carries the simulated p95 of the
+    active fleet.  ``log_evals`` keeps the winning chain's per-step log of the last
+    Clover re-plan (evals.csv)."""
     import torch
     from .search import anneal_chains, base_config, co2opt_config
     if scheme not in SCHEMES:
@@ -114,6 +125,20 @@ def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, pro
         w = base_w.copy()
     fleet = engine.realize(ConfigGraph(w, profile.variant_count, profile.name), n)
     rep = TimelineReport()
+    des_cache: dict = {}
+    l_tail_des = None
+    if des_window_s > 0:
+        from .sim import Workload, simulate_fleets
+        from .search import base_config as _bc
+        des_w = Workload(base_sc.arrival_rps, float(des_window_s), derive_seed(seed, 0x5EED))
+        l_tail_des = simulate_fleets([_bc(n, profile)], profile, des_w, engine=engine)[0].p95_ms
+
+        def des_p95(fleets):
+            todo = [f for f in fleets if f not in des_cache]
+            if todo:
+                for f, r in zip(todo, simulate_fleets(todo, profile, des_w, l_tail_des, engine=engine)):
+                    des_cache[f] = r.p95_ms
+            return [des_cache[f] for f in fleets]
     prev_ci = 0.0
     cum, cum_base, acc_sum = 0.0, 0.0, 0.0
     steps = int(round((trace.samples[-1][0] - trace.samples[0][0]) / cp.trace_step_s)) + 1
@@ -133,11 +158,19 @@ def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, pro
             if scheme == "clover":
                 starts = np.repeat(w[None, :].astype(np.uint16), chains, axis=0)
                 res = anneal_chains(engine, starts, profile, sc, ap, tick_seed, chain_base=chain_base,
-                                    group=group)
+                                    group=group, log=log_evals)
                 cand_w = np.asarray(res.best.graph.weights, dtype=np.int64)
                 cand = dict(f=res.best.f_value, h=res.best.h_value, p95_ms=res.best.p95_ms,
                             sla_met=res.best.sla_met)
                 evals = res.evals
+                if log_evals and res.log is not None:
+                    loc = res.best_chain - chain_base
+                    rep.evals_log = res.log[loc:loc + 1]
+                    rep.evals_steps = [int(res.results[loc]["steps"])]
+                if des_window_s > 0:
+                    cand_w, cand, des_evals = _des_confirm(engine, profile, n, res, des_p95, l_tail_des, des_top,
+                                                           cand_w, cand)
+                    evals += des_evals
             elif scheme == "oracle":
                 o = engine.oracle_search(profile, sc)
                 cid, assign = engine.oracle_decode(profile, o["index"])
@@ -178,9 +211,12 @@ def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, pro
         cum += reqs * g_req
         cum_base += reqs * base["energy_wh"] / 1000.0 * ci * pue
         acc_sum += act["accuracy"]
-        rep.rows.append(dict(t=t, ci=ci, scheme=scheme, p95_ms=act["p95_ms"], sla_met=bool(act["sla_met"]),
-                             accuracy=act["accuracy"], gco2_per_request=g_req, cumulative_gco2=cum,
-                             optimizing=optimizing))
+        row = dict(t=t, ci=ci, scheme=scheme, p95_ms=act["p95_ms"], sla_met=bool(act["sla_met"]),
+                   accuracy=act["accuracy"], gco2_per_request=g_req, cumulative_gco2=cum, optimizing=optimizing)
+        if des_window_s > 0:
+            dp = des_p95([fleet])[0]
+            row.update(des_p95_ms=dp, des_sla_met=bool(dp <= l_tail_des))
+        rep.rows.append(row)
     tts = [r.device_ms for r in rep.replans]
     rep.summary = dict(
         scheme=scheme, n_gpus=n, ticks=steps, replans=len(rep.replans), total_gco2=cum,
@@ -194,4 +230,33 @@ def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, pro
         candidates_scored=int(sum(r.evals for r in rep.replans)),
         reconfigured_gpus=int(sum(r.changed_gpus for r in rep.replans)),
         downtime_gpu_s=float(sum(r.changed_gpus for r in rep.replans) * cp.reconfig_downtime_s))
+    if des_window_s > 0:
+        rep.summary.update(des_window_s=float(des_window_s), des_l_tail_ms=l_tail_des,
+                           des_sla_violation_ticks=sum(1 for r in rep.rows if not r["des_sla_met"]),
+                           des_simulations=len(des_cache))
     return rep
+
+
+def _des_confirm(engine, profile, n, res, des_p95, l_tail_des, top, cand_w, cand):
+    """Simulate the best distinct chain winners; keep the first (surrogate order) whose
+    simulated p95 meets L_tail_DES.  Returns (graph, candidate dict, simulations run)."""
+    order = np.lexsort((np.arange(len(res.results)), res.results["h"], res.results["sla_met"] == 0))
+    graphs, rows, seen = [], [], set()
+    for c in order:
+        key = res.best_w[c].tobytes()
+        if key in seen or res.results[c]["status"] < 0:
+            continue
+        seen.add(key)
+        graphs.append(res.best_w[c].astype(np.int64))
+        rows.append(res.results[c])
+        if len(graphs) >= top:
+            break
+    fleets = [engine.realize(ConfigGraph(g, profile.variant_count, profile.name), n) for g in graphs]
+    p95s = des_p95(fleets)
+    for g, r, p in zip(graphs, rows, p95s):
+        if p <= l_tail_des:
+            return g, dict(f=float(r["f"]), h=float(r["h"]), p95_ms=float(r["p95_ms"]), sla_met=bool(r["sla_met"]),
+                           des_p95_ms=p), len(fleets)
+    cand = dict(cand)
+    cand["sla_met"] = False                  # no simulated winner meets the SLA: keep the incumbent
+    return cand_w, cand, len(fleets)

@@ -165,6 +165,104 @@ class ProfileTable:
         }
 
 
+PROFILE_SECTIONS = ("variants", "latency", "energy", "idle")
+
+
+def profile_from_dict(doc: Mapping, topology: MigTopology = DEFAULT_TOPOLOGY) -> ProfileTable:
+    """Key/value profile document -> ProfileTable.
+
+    Sections ``variants`` (id, accuracy, memory_gb[, name]), ``latency`` (variant,
+    slice, mean_service_ms, dist[, sigma]), ``energy`` (variant, slice,
+    wh_per_request), ``idle`` (slice, watts).  Schema violations, duplicate
+    (variant, slice) rows and non-monotone accuracy raise ProfileError.
+    """
+    if not isinstance(doc, Mapping):
+        raise ProfileError("profile document must be a key/value mapping")
+    for sec in PROFILE_SECTIONS:
+        if sec not in doc or not isinstance(doc[sec], (list, tuple)):
+            raise ProfileError("profile section %r missing or not a list" % sec)
+
+    def field_of(row, key, kind, sec):
+        if not isinstance(row, Mapping) or key not in row:
+            raise ProfileError("%s row lacks field %r" % (sec, key))
+        try:
+            return kind(row[key])
+        except (TypeError, ValueError) as exc:
+            raise ProfileError("%s.%s: %s" % (sec, key, exc)) from exc
+
+    def slice_of(row, sec):
+        label = field_of(row, "slice", str, sec)
+        try:
+            return SliceType.from_label(label)
+        except Exception as exc:
+            raise ProfileError("%s: unknown slice %r" % (sec, label)) from exc
+
+    variants = []
+    seen_v = set()
+    for row in doc["variants"]:
+        vid = field_of(row, "id", int, "variants")
+        if vid in seen_v:
+            raise ProfileError("duplicate variant id %d" % vid)
+        seen_v.add(vid)
+        variants.append(VariantSpec(vid, field_of(row, "accuracy", float, "variants"),
+                                    field_of(row, "memory_gb", float, "variants"),
+                                    str(row.get("name", "")) if isinstance(row, Mapping) else ""))
+    lat: dict = {}
+    for row in doc["latency"]:
+        key = (field_of(row, "variant", int, "latency"), slice_of(row, "latency"))
+        if key in lat:
+            raise ProfileError("duplicate latency row (v%d, %s)" % (key[0], key[1].label))
+        dist = field_of(row, "dist", str, "latency")
+        sigma = float(row.get("sigma", 0.0) or 0.0)
+        lat[key] = (field_of(row, "mean_service_ms", float, "latency"), dist, sigma)
+    energy: dict = {}
+    for row in doc["energy"]:
+        key = (field_of(row, "variant", int, "energy"), slice_of(row, "energy"))
+        if key in energy:
+            raise ProfileError("duplicate energy row (v%d, %s)" % (key[0], key[1].label))
+        energy[key] = field_of(row, "wh_per_request", float, "energy")
+    idle: dict = {}
+    for row in doc["idle"]:
+        s = slice_of(row, "idle")
+        if s in idle:
+            raise ProfileError("duplicate idle row %s" % s.label)
+        idle[s] = field_of(row, "watts", float, "idle")
+    if set(lat) != set(energy):
+        raise ProfileError("latency and energy rows cover different (variant, slice) pairs")
+    missing = [s.label for s in SLICE_ORDER if s not in idle]
+    if missing:
+        raise ProfileError("idle rows missing for %s" % ",".join(missing))
+    service = {k: ServiceRow(m, d, sg, energy[k]) for k, (m, d, sg) in lat.items()}
+    return ProfileTable(str(doc.get("name", "profile")), variants, service, idle, topology)
+
+
+def load_profiles(path: str, topology: MigTopology = DEFAULT_TOPOLOGY) -> ProfileTable:
+    """load_profiles(path) -> ProfileTable: a JSON (or YAML) key/value document."""
+    import json
+    try:
+        with open(path, "r", encoding="utf-8") as fh:
+            text = fh.read()
+    except OSError as exc:
+        raise ProfileError("cannot read profile %s: %s" % (path, exc)) from exc
+    try:
+        doc = json.loads(text)
+    except ValueError:
+        try:
+            import yaml
+            doc = yaml.safe_load(text)
+        except Exception as exc:
+            raise ProfileError("profile %s is neither JSON nor YAML: %s" % (path, exc)) from exc
+    return profile_from_dict(doc, topology)
+
+
+def save_profile(profile: ProfileTable, path: str) -> None:
+    """Serialise a ProfileTable (round-trips through load_profiles)."""
+    import json
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        json.dump(profile.to_json_dict(), fh, indent=1, sort_keys=False)
+        fh.write("\n")
+
+
 def _pow2_scale(max_value: float, bits: int = 31) -> int:
     """Largest k such that max_value * 2**k < 2**bits (k may be negative)."""
     if max_value <= 0:

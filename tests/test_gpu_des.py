@@ -140,3 +140,27 @@ def test_large_fleet_properties(engine):
         assert abs(S.overall_accuracy(r, p) - r.accuracy) <= 1e-15
     base = reps[-1]
     assert abs(base.accuracy - p.accuracy(p.variant_count)) <= 1e-15
+
+
+def test_run_trace_with_des_confirmation(engine, tmp_path):
+    """SPEC acceptance 6 analogue with the simulator as the judge: every steady-state tick of the
+    DES-confirmed Clover controller serves a fleet whose simulated p95 meets L_tail_DES."""
+    from paper_2304_09781_b200.controller import ControllerParams, run_trace
+    from paper_2304_09781_b200.objective import AnnealParams
+    from paper_2304_09781_b200.profiles import synthetic_trace
+    from paper_2304_09781_b200 import reports as R
+    prof = synthetic_profile("efficientnet")
+    tr = synthetic_trace(hours=2.0)
+    ap = AnnealParams(proposal="uniform", max_steps=16)
+    rep = run_trace(engine, tr, "clover", 8, prof, 0.5, ap, ControllerParams(), seed=3, chains=16,
+                    des_window_s=120.0, des_top=8, log_evals=True)
+    assert rep.summary["des_l_tail_ms"] > 0 and rep.summary["des_simulations"] >= 1
+    assert all(r["des_sla_met"] for r in rep.rows)
+    assert rep.summary["replans"] >= 1 and rep.evals_log is not None
+    R.write_trace_run(str(tmp_path), rep)
+    lines = open(tmp_path / "evals.csv").read().splitlines()
+    assert lines[0] == ",".join(R.EVAL_FIELDS) and len(lines) == 1 + rep.evals_steps[0]
+    again = run_trace(engine, tr, "clover", 8, prof, 0.5, ap, ControllerParams(), seed=3, chains=16,
+                      des_window_s=120.0, des_top=8)
+    R.write_timeline_csv(str(tmp_path / "t2.csv"), again)
+    assert open(tmp_path / "t2.csv").read() == open(tmp_path / "timeline.csv").read()
