@@ -109,6 +109,8 @@ typedef struct clv_chain_result {
     int32_t best_step;       /* -1 = the start graph */
     int64_t best_index;      /* canonical neighbour index at best_step, -1 = start */
     int64_t evals;           /* candidates scored by this chain (start included) */
+    int64_t edge_evals;      /* sum over steps of (non-zero edges of the centre x candidates scored):
+                                the E_nz factor of the per-candidate work */
 } clv_chain_result;
 
 /* One row of the optional per-step log (SPEC:487 schema). */

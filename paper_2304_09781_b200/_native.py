@@ -39,7 +39,7 @@ class AnnealParamsC(ctypes.Structure):
 class ChainResult(ctypes.Structure):
     _fields_ = [("f", c_f64), ("h", c_f64), ("p95_ms", c_f64), ("accuracy", c_f64),
                 ("energy_wh", c_f64), ("sla_met", c_i32), ("status", c_i32), ("steps", c_i32),
-                ("best_step", c_i32), ("best_index", c_i64), ("evals", c_i64)]
+                ("best_step", c_i32), ("best_index", c_i64), ("evals", c_i64), ("edge_evals", c_i64)]
 
 
 class LogRow(ctypes.Structure):

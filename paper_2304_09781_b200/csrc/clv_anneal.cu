@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     unsigned int bk1 = 0;
     unsigned long long bk2 = 0;
     int best_step = -1, stall = 0, steps = 0, status = 0;
-    long long best_idx = -1, evals = 1;
+    long long best_idx = -1, evals = 1, edge_evals = 0;
     if (tid == 0) {
         int invalid = 0;
         long long tot = 0;
@@ -387,6 +387,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             if (s.w[e] > 0 && !((s.mem_ok >> e) & 1ULL)) invalid = 1;
         }
         if (tot < 1 || !feasible(args.F, n, s.svec[0], s.svec[1], s.svec[2], s.svec[3], s.svec[4])) invalid = 1;
+        edge_evals = __popcll(s.pmask);
         const Score sc = epilogue_d(s.S[0], s.S[1], s.S[2], s.S[3], lmax_of(s, s.pmask), s.ec);
         hc = sc.h;
         bk1 = sc.sla ? 0u : 1u; bk2 = okey(sc.h);
@@ -521,6 +522,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 bool slap = false;
                 if (MODE == MODE_UNIFORM_PROPOSAL) {
                     evals += 1;
+                    edge_evals += (long long)s.nPE;
                     int r1, r2, a1, a2;
                     decode_move(s, E, Pr.idx, r1, r2, a1, a2);
                     const Score sp = score_move(s, r1, r2, a1, a2);
@@ -529,6 +531,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                     ck1 = sp.sla ? 0u : 1u; ck2 = okey(sp.h); cidx = Pr.idx;
                 } else {
                     evals += (long long)total;
+                    edge_evals += (long long)s.nPE * (long long)total;
                     // best-tracking candidate: SLA-meeting first
                     if (Sr.idx != 0x7FFFFFFF) { ck1 = 0u; ck2 = Sr.key; cidx = Sr.idx; }
                     else { ck1 = 1u; ck2 = Vr.key; cidx = Vr.idx; }
@@ -607,7 +610,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         r.f = sb.f; r.h = sb.h; r.p95_ms = sb.L; r.accuracy = sb.A; r.energy_wh = sb.E;
         r.sla_met = sb.sla;
         r.status = status; r.steps = steps; r.best_step = best_step;
-        r.best_index = best_idx; r.evals = evals;
+        r.best_index = best_idx; r.evals = evals; r.edge_evals = edge_evals;
         args.res[chain] = r;
     }
 }

@@ -49,7 +49,7 @@ def eval_params(s: Scenario) -> N.EvalParams:
 class AnnealBatch:
     """Device-resident results of one clv_anneal launch (torch tensors on the GPU)."""
 
-    results: object        # uint8 [n_chains * 72] viewed through CHAIN_DTYPE on host
+    results: object        # uint8 [n_chains * 80] viewed through CHAIN_DTYPE on host
     best_w: object         # uint16 [n_chains, E]
     final_w: object        # uint16 [n_chains, E]
     log: object            # optional uint8 [n_chains * max_steps * 56]
@@ -68,12 +68,13 @@ class AnnealBatch:
 
 CHAIN_DTYPE = np.dtype([("f", "<f8"), ("h", "<f8"), ("p95_ms", "<f8"), ("accuracy", "<f8"),
                         ("energy_wh", "<f8"), ("sla_met", "<i4"), ("status", "<i4"), ("steps", "<i4"),
-                        ("best_step", "<i4"), ("best_index", "<i8"), ("evals", "<i8")])
+                        ("best_step", "<i4"), ("best_index", "<i8"), ("evals", "<i8"),
+                        ("edge_evals", "<i8")])
 LOG_DTYPE = np.dtype([("temp", "<f8"), ("f", "<f8"), ("h", "<f8"), ("p95_ms", "<f8"), ("iter", "<i4"),
                       ("ged_from_center", "<i4"), ("sla_met", "<i4"), ("accepted", "<i4"),
                       ("new_best", "<i4"), ("n_neighbours", "<i4")])
 RECORD_DTYPE = np.dtype([("k1", "<u8"), ("k2", "<u8"), ("index", "<i8"), ("h", "<f8")])
-assert CHAIN_DTYPE.itemsize == ctypes.sizeof(N.ChainResult) == 72
+assert CHAIN_DTYPE.itemsize == ctypes.sizeof(N.ChainResult) == 80
 assert LOG_DTYPE.itemsize == ctypes.sizeof(N.LogRow) == 56
 assert RECORD_DTYPE.itemsize == ctypes.sizeof(N.Record) == 32
 
@@ -341,7 +342,7 @@ class CloverEngine:
                               1 if ap.proposal == "uniform" else 0, 1 if ap.evaluate == "proposal" else 0)
         steps = ap.step_limit()
         if out is None or out.n_chains != n_chains or (log and out.log is None):
-            out = AnnealBatch(torch.empty(n_chains * 72, dtype=torch.uint8, device=dev),
+            out = AnnealBatch(torch.empty(n_chains * CHAIN_DTYPE.itemsize, dtype=torch.uint8, device=dev),
                               torch.empty((n_chains, E), dtype=torch.uint16, device=dev),
                               torch.empty((n_chains, E), dtype=torch.uint16, device=dev),
                               torch.zeros(max(1, n_chains * steps * 56), dtype=torch.uint8, device=dev) if log else None,
