@@ -409,7 +409,7 @@ int clv_score_graphs(clv_ctx *ctx, int family, const uint16_t *w_dev, int64_t co
     a.count = count; a.index_base = index_base; a.w = w_dev; a.topo = ctx->topo_dev;
     a.f_out = f_dev; a.h_out = h_dev; a.p95_out = p95_dev; a.sla_out = sla_dev; a.feas_out = feas_dev;
     a.sel = make_sel(ctx);
-    CLV_CUDA(launch_score_graphs(a, grid_for(ctx, count, 256), st), "score_graphs");
+    CLV_CUDA(launch_score_graphs(a, ctx->fam[family], grid_for(ctx, count, 256), st), "score_graphs");
     if (!best) return CLV_OK;
     return fetch_best(ctx, select_mode, st, best);
 }

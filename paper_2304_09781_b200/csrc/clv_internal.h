@@ -194,7 +194,7 @@ cudaError_t launch_feasible(FeasView F, int n, const int32_t *vec5, long long co
                             cudaStream_t s);
 cudaError_t launch_realize(FeasView F, const Topology *topo_dev, int n, const int32_t *vec5_dev,
                            int32_t *parts_dev, cudaStream_t s);
-cudaError_t launch_score_graphs(const ScoreArgs &a, int grid, cudaStream_t s);
+cudaError_t launch_score_graphs(const ScoreArgs &a, const FamilyTables &T, int grid, cudaStream_t s);
 cudaError_t launch_score_x(const ScoreArgs &a, int n, int grid, cudaStream_t s);
 cudaError_t launch_oracle(const OracleArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_anneal(const AnnealArgs &a, int cluster, cudaStream_t s);

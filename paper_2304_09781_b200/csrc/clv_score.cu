@@ -9,6 +9,7 @@
 //                 (shuffle prefix-sum of slices per GPU, mig.py:286-296)
 //  oracle       : index -> (config id, mixed-radix variant digits)
 //  sweep        : index -> counter-RNG draws -> per-pod graphs
+#include <algorithm>
 #include "clv_internal.h"
 
 namespace clv {
@@ -119,11 +120,210 @@ __global__ void __launch_bounds__(SNT) score_graphs_kernel(const __grid_constant
     grid_finish<SNT>(r0, r1, c_valid, c_sla, a.sel);
 }
 
-cudaError_t launch_score_graphs(const ScoreArgs &a, int grid, cudaStream_t s) {
-    const int E = 0;  (void)E;
-    bool vec = (reinterpret_cast<uintptr_t>(a.w) % 16) == 0;
-    if (vec) score_graphs_kernel<true><<<grid, SNT, 0, s>>>(a);
-    else score_graphs_kernel<false><<<grid, SNT, 0, s>>>(a);
+// TMA-pipelined variant (16-B aligned input): one elected thread streams full
+// 256-candidate tiles (256 * 5V * 2 B, a multiple of 16) into a GS-stage shared
+// ring with cp.async.bulk + mbarrier complete_tx, so GS-1 tiles are in flight
+// while the CTA scores the current one.  Per candidate: exact fp64 FMAs of the
+// three per-edge rows (integers < 2^53: exact in any order, = the int64 sums),
+// slice counts and the latency-rank presence mask; the idle row is per slice,
+// so S_idle = sum_s count_s * idle_s after the loop.
+constexpr int GS = 3;                       // pipeline stages
+constexpr int CPT = 2;                      // candidates per thread
+constexpr int GT = SNT * CPT;               // candidates per tile
+constexpr int PCH = 7;                      // presence-mask chunk (bits)
+constexpr int NPCH = (CLV_MAX_EDGES + PCH - 1) / PCH;
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile("{\n\t.reg .pred P;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+                 "@!P bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// Per-family rows as kernel parameters (constant bank): with the edge loop fully
+// unrolled (template on V) every row value is a compile-time constant-bank operand.
+struct GraphRows {
+    double thr[CLV_MAX_EDGES], acc[CLV_MAX_EDGES], en[CLV_MAX_EDGES];
+    double idle[CLV_K];
+    unsigned long long bad;                 // bit e: edge e is memory-infeasible
+};
+
+// The p95 of a graph is the largest lat95 over its present edges: the present-edge
+// mask is split into 7-bit chunks and each chunk's maximum comes from a 128-entry
+// table (shared memory), so the per-edge work is one predicate-set bit.
+template <int V>
+__global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_constant__ ScoreArgs a,
+                                                               const __grid_constant__ GraphRows R) {
+    constexpr int E = V * CLV_K;
+    constexpr int NC = (E + PCH - 1) / PCH;
+    extern __shared__ __align__(128) unsigned char gsm[];
+    __shared__ __align__(8) unsigned long long full[GS];
+    __shared__ double chunk_max[NC][1 << PCH];
+    uint16_t *ring = reinterpret_cast<uint16_t *>(gsm);
+    {
+        const FamilyTables &T = *a.fam;
+        for (int q = threadIdx.x; q < NC * (1 << PCH); q += SNT) {
+            const int c = q >> PCH, bits = q & ((1 << PCH) - 1);
+            double mx = 0.0;
+            for (int b = 0; b < PCH; ++b) {
+                const int e = c * PCH + b;
+                if (e < E && ((bits >> b) & 1)) mx = mx > T.lat95[e] ? mx : T.lat95[e];
+            }
+            chunk_max[c][bits] = mx;
+        }
+    }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < GS; ++q) mbar_init(&full[q], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long ntiles = (a.count + GT - 1) / GT;
+    const int n = a.ec.n;
+    // tile j of this CTA is global tile blockIdx.x + j * gridDim.x
+    auto issue = [&](long long j) {
+        const long long tile = blockIdx.x + j * gridDim.x;
+        if (tile >= ntiles) return;
+        const long long rows = min((long long)GT, a.count - tile * GT);
+        const unsigned bytes = (unsigned)(((size_t)rows * E * 2) & ~(size_t)15);
+        const int st = (int)(j % GS);
+        // the stage was last touched through the generic proxy (reads, tail stores)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[st], bytes);
+        if (bytes) bulk_g2s(ring + (size_t)st * GT * E, a.w + (size_t)tile * GT * E, bytes, &full[st]);
+    };
+    if (threadIdx.x == 0)
+        for (int q = 0; q < GS - 1; ++q) issue(q);
+    RecP r0 = recp_none(), r1 = recp_none();
+    unsigned long long c_valid = 0, c_sla = 0;
+    for (long long j = 0;; ++j) {
+        const long long tile = blockIdx.x + j * gridDim.x;
+        if (tile >= ntiles) break;
+        if (threadIdx.x == 0) issue(j + GS - 1);
+        const int st = (int)(j % GS);
+        const long long rows = min((long long)GT, a.count - tile * GT);
+        uint16_t *buf = ring + (size_t)st * GT * E;
+        mbar_wait(&full[st], (unsigned)((j / GS) & 1));
+        {   // elements the bulk copy left out (tail of the last, partial tile)
+            const size_t done = (((size_t)rows * E * 2) & ~(size_t)15) / 2;
+            const size_t tot = (size_t)rows * E;
+            if (done < tot) {
+                for (size_t q = done + threadIdx.x; q < tot; q += SNT) buf[q] = a.w[(size_t)tile * GT * E + q];
+                __syncthreads();
+            }
+        }
+        double S0[CPT], S1[CPT], S2[CPT];
+        int sv[CPT][CLV_K];
+        unsigned long long pe[CPT];
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            S0[c] = S1[c] = S2[c] = 0.0;
+            pe[c] = 0ULL;
+#pragma unroll
+            for (int k = 0; k < CLV_K; ++k) sv[c][k] = 0;
+        }
+        const uint16_t *w0 = buf + threadIdx.x * E;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const int x = w0[c * SNT * E + e];
+                const double xd = (double)x;
+                S0[c] = __fma_rn(xd, R.thr[e], S0[c]);
+                S1[c] = __fma_rn(xd, R.acc[e], S1[c]);
+                S2[c] = __fma_rn(xd, R.en[e], S2[c]);
+                sv[c][e % CLV_K] += x;
+                pe[c] |= (unsigned long long)(x != 0) << e;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            const int local = threadIdx.x + c * SNT;
+            if (local >= rows) continue;
+            double S3 = 0.0;
+#pragma unroll
+            for (int k = 0; k < CLV_K; ++k) S3 = __fma_rn((double)sv[c][k], R.idle[k], S3);
+            double lmax = 0.0;
+#pragma unroll
+            for (int q = 0; q < NC; ++q) {
+                const double v = chunk_max[q][(pe[c] >> (q * PCH)) & ((1 << PCH) - 1)];
+                lmax = lmax > v ? lmax : v;
+            }
+            const long long i = tile * GT + local;
+            const bool feas = !(pe[c] & R.bad) && pe[c] != 0 &&
+                              feasible(a.F, n, sv[c][0], sv[c][1], sv[c][2], sv[c][3], sv[c][4]);
+            if (feas) {
+                Score sc = epilogue_d(S0[c], S1[c], S2[c], S3, lmax, a.ec);
+                ++c_valid;
+                c_sla += sc.sla;
+                consider(r0, r1, sc, a.index_base + i, a.select_mode);
+                if (a.f_out) a.f_out[i] = sc.f;
+                if (a.h_out) a.h_out[i] = sc.h;
+                if (a.p95_out) a.p95_out[i] = sc.L;
+                if (a.sla_out) a.sla_out[i] = sc.sla;
+            } else {
+                const double nan = __longlong_as_double(0x7FF8000000000000LL);
+                if (a.f_out) a.f_out[i] = nan;
+                if (a.h_out) a.h_out[i] = nan;
+                if (a.p95_out) a.p95_out[i] = nan;
+                if (a.sla_out) a.sla_out[i] = 0;
+            }
+            if (a.feas_out) a.feas_out[i] = feas;
+        }
+        __syncthreads();                     // stage st is free again (re-armed GS-1 tiles later)
+    }
+    grid_finish<SNT>(r0, r1, c_valid, c_sla, a.sel);
+}
+
+template <int V>
+static cudaError_t launch_tma(const ScoreArgs &a, const GraphRows &R, cudaStream_t s) {
+    auto kern = score_graphs_tma_kernel<V>;
+    const size_t smem = (size_t)GS * GT * V * CLV_K * 2;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SNT, smem);
+    const long long tiles = (a.count + GT - 1) / GT;
+    const long long g = std::max(1LL, std::min(tiles, (long long)sms * std::max(occ, 1)));
+    kern<<<(unsigned)g, SNT, smem, s>>>(a, R);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_score_graphs(const ScoreArgs &a, const FamilyTables &T, int grid, cudaStream_t s) {
+    const bool aligned = (reinterpret_cast<uintptr_t>(a.w) % 16) == 0;
+    if (aligned) {
+        GraphRows R{};
+        for (int e = 0; e < T.E; ++e) {
+            R.thr[e] = (double)T.thr_q[e]; R.acc[e] = (double)T.acc_q[e]; R.en[e] = (double)T.en_q[e];
+            if (!((T.mem_ok >> e) & 1ULL)) R.bad |= 1ULL << e;
+        }
+        for (int k = 0; k < CLV_K; ++k) R.idle[k] = (double)T.idle_q[k];
+        switch (T.V) {
+            case 1: return launch_tma<1>(a, R, s);
+            case 2: return launch_tma<2>(a, R, s);
+            case 3: return launch_tma<3>(a, R, s);
+            case 4: return launch_tma<4>(a, R, s);
+            case 5: return launch_tma<5>(a, R, s);
+            case 6: return launch_tma<6>(a, R, s);
+            case 7: return launch_tma<7>(a, R, s);
+            default: return launch_tma<8>(a, R, s);
+        }
+    }
+    score_graphs_kernel<false><<<grid, SNT, 0, s>>>(a);
     return cudaGetLastError();
 }
 
