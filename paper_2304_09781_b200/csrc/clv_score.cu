@@ -469,25 +469,40 @@ cudaError_t launch_oracle(const OracleArgs &a, int grid, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------- sweep
+// The candidate's counter stream (oracle/rng.py::Stream): 32-bit draws, low then
+// high half of splitmix64 word j of the stream keyed by h0.  The word base
+// h0 + (j+1)*golden is advanced incrementally instead of multiplied out.
 struct Draws {
-    uint64_t h0, word;
+    uint64_t zb, word;
     uint32_t j;
+    __device__ inline void init(uint64_t h0) { zb = h0; word = 0; j = 0; }
     __device__ inline uint32_t next() {
         uint32_t out;
-        if ((j & 1u) == 0) { word = stream_word(h0, j >> 1); out = (uint32_t)word; }
-        else out = (uint32_t)(word >> 32);
+        if ((j & 1u) == 0) {
+            zb += 0x9E3779B97F4A7C15ULL;
+            uint64_t z = zb;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+            word = z ^ (z >> 31);
+            out = (uint32_t)word;
+        } else {
+            out = (uint32_t)(word >> 32);
+        }
         ++j;
         return out;
     }
-    __device__ inline int bounded(uint32_t k) {
-        return (int)(((uint64_t)next() * k) >> 32);
-    }
 };
 
+struct __align__(32) SRow {
+    double thr, acc, en, idle;
+};
+
+constexpr int ZROW = CLV_MAX_EDGES;           // all-zero row: a configuration draw adds nothing
+
 __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ SweepArgs a) {
-    __shared__ ERow row[CLV_MAX_PODS][CLV_MAX_EDGES];
+    __shared__ SRow row[CLV_MAX_PODS][CLV_MAX_EDGES + 1];
+    __shared__ unsigned long long rbit[CLV_MAX_PODS][CLV_MAX_EDGES + 1];
     __shared__ double lat_by_rank[CLV_MAX_PODS][CLV_MAX_EDGES];
-    __shared__ unsigned char rank[CLV_MAX_PODS][CLV_MAX_EDGES];
     __shared__ unsigned char nfeas[CLV_MAX_PODS][CLV_K];
     __shared__ unsigned char flist[CLV_MAX_PODS][CLV_K][CLV_MAX_VARIANTS];
     __shared__ unsigned char nsl[CLV_MAX_CONFIGS];
@@ -495,7 +510,15 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
     const Topology &P = *a.topo;
     for (int p = 0; p < a.n_pods; ++p) {
         const FamilyTables &T = a.fam[a.pods[p].family];
-        stage_rows(row[p], lat_by_rank[p], rank[p], T);
+        for (int e = threadIdx.x; e <= CLV_MAX_EDGES; e += SNT) {
+            const bool real = e < T.E;
+            row[p][e].thr = real ? (double)T.thr_q[e] : 0.0;
+            row[p][e].acc = real ? (double)T.acc_q[e] : 0.0;
+            row[p][e].en = real ? (double)T.en_q[e] : 0.0;
+            row[p][e].idle = real ? (double)T.idle_q[e % 5] : 0.0;
+            rbit[p][e] = real ? (1ULL << T.rank[e]) : 0ULL;
+            if (e < CLV_MAX_EDGES) lat_by_rank[p][e] = T.lat_by_rank[e];
+        }
         for (int t = threadIdx.x; t < CLV_K * CLV_MAX_VARIANTS; t += SNT) {
             flist[p][t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS] = T.feas_list[t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS];
             if (t < CLV_K) nfeas[p][t] = T.nfeas[t];
@@ -512,25 +535,35 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
     for (long long i = a.begin + (long long)blockIdx.x * SNT + threadIdx.x; i < a.end;
          i += (long long)gridDim.x * SNT) {
         Draws d;
-        d.h0 = derive_seed2(a.seed, (uint64_t)i);
-        d.j = 0; d.word = 0;
+        d.init(derive_seed2(a.seed, (uint64_t)i));
         double f = 0.0, h = 0.0;
         bool sla = true;
         for (int p = 0; p < a.n_pods; ++p) {
-            long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+            // fp64 sums of exact integers (< 2^53): identical to the oracle's int64 sums
+            double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
             unsigned long long m = 0;
-            for (int g = 0; g < a.pods[p].n_gpus; ++g) {
-                const int r = d.bounded(K);
-                const int ns = nsl[r];
-                for (int j = 0; j < ns; ++j) {
-                    const int k = kinds[r][j];
-                    const int v = flist[p][k][d.bounded(nfeas[p][k])];
-                    const int e = v * 5 + k;
-                    S0 += row[p][e].thr; S1 += row[p][e].acc; S2 += row[p][e].en; S3 += row[p][e].idle;
-                    m |= 1ULL << rank[p][e];
-                }
+            // One draw per iteration, in the oracle's order (oracle/search.py::draw_candidate):
+            // a configuration draw when the current GPU's slices are exhausted, else the next
+            // slice's variant draw.  The body is branch-free (a configuration draw adds the
+            // all-zero row), so lanes stay converged until their last GPU.
+            const int ng = a.pods[p].n_gpus;
+            int g = 0, rem = 0, r = 0, slot = 0;
+            while (rem != 0 || g < ng) {
+                const uint32_t w = d.next();
+                const bool cfg = rem == 0;
+                const int k = kinds[r][slot & 7];
+                const int v = flist[p][k][(int)(((uint64_t)w * nfeas[p][k]) >> 32)];
+                const int e = cfg ? ZROW : v * 5 + k;
+                const SRow &q = row[p][e];
+                S0 += q.thr; S1 += q.acc; S2 += q.en; S3 += q.idle;
+                m |= rbit[p][e];
+                const int rn = (int)(((uint64_t)w * K) >> 32);
+                r = cfg ? rn : r;
+                rem = cfg ? (int)nsl[rn] : rem - 1;
+                slot = cfg ? 0 : slot + 1;
+                g += cfg ? 1 : 0;
             }
-            Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[p][63 - __clzll((long long)m)], a.pods[p].ec);
+            Score sc = epilogue_d(S0, S1, S2, S3, lat_by_rank[p][63 - __clzll((long long)m)], a.pods[p].ec);
             const double wt = a.pods[p].weight;
             if (p == 0) { f = wt * sc.f; h = wt * sc.h; }
             else { f = f + wt * sc.f; h = h + wt * sc.h; }
