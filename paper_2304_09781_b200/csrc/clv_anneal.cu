@@ -289,16 +289,20 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
 }
 
 // Exact score of one neighbour folded into the thread's records.
-template <int MODE>
-__device__ __forceinline__ void fold(const AnnealSmem &s, double t, double ac, double en, double id, double lmax,
-                                     int idx, KRec &rS, KRec &rV, KRec &rP, uint64_t seed, uint64_t gchain,
-                                     uint64_t k) {
+template <int MODE, bool EC1>
+__device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args, double t, double ac, double en,
+                                     double id, double lmax, int idx, KRec &rS, KRec &rV, KRec &rP, uint64_t seed,
+                                     uint64_t gchain, uint64_t k) {
     if (MODE == MODE_UNIFORM_PROPOSAL) {
         const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
         if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; }
         return;
     }
-    const Score sc = epilogue_d(t, ac, en, id, lmax, s.ec);
+    // one evaluation scenario for every chain: its constants are kernel parameters
+    // (constant-bank operands); per-chain scenarios come from the CTA's shared copy
+    Score sc;
+    if constexpr (EC1) sc = epilogue_d(t, ac, en, id, lmax, args.ec0);
+    else sc = epilogue_d(t, ac, en, id, lmax, s.ec);
     const unsigned long long key = okey(sc.h);
     if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; } }
     else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; } }
@@ -317,7 +321,9 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, double t, double ac, d
         prof_last = _now;                                                              \
     }
 
-template <int MODE, int MINB, int UNR, bool PROF = false>
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }   // finite operands
+
+template <int MODE, int MINB, int UNR, bool PROF = false, bool EC1 = false>
 __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
     long long prof_acc[7] = {0, 0, 0, 0, 0, 0, 0};
     long long prof_last = 0;
@@ -418,8 +424,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (a != R.r1 && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]]) {
                     ++cnt;
                     const ARow &A = s.row[a];
-                    fold<MODE>(s, s.S[0] + R.d0 + A.thr, s.S[1] + R.d1 + A.acc, s.S[2] + R.d2 + A.en,
-                               s.S[3] + R.d3 + A.idle, fmax(s.lat_by_rank[R.top], s.lat_e[a]), (int)R.p * E + a,
+                    fold<MODE, EC1>(s, args, s.S[0] + R.d0 + A.thr, s.S[1] + R.d1 + A.acc, s.S[2] + R.d2 + A.en,
+                               s.S[3] + R.d3 + A.idle, dmax(s.lat_by_rank[R.top], s.lat_e[a]), (int)R.p * E + a,
                                rS, rV, rP, args.seed, gchain, (uint64_t)k);
                 }
                 i += dI; a += dA;
@@ -456,9 +462,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                                 ++cnt;
                                 const int a1 = ent & 63, a2 = (ent >> 6) & 63;
                                 const ARow &A1 = s.row[a1], &A2 = s.row[a2];
-                                fold<MODE>(s, s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
+                                fold<MODE, EC1>(s, args, s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
                                            s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
-                                           fmax(s.lat_by_rank[R.top], fmax(s.lat_e[a1], s.lat_e[a2])),
+                                           dmax(s.lat_by_rank[R.top], dmax(s.lat_e[a1], s.lat_e[a2])),
                                            E * E + (int)R.p * NPc + (int)(ent >> 17), rS, rV, rP, args.seed,
                                            gchain, (uint64_t)k);
                             }
@@ -617,7 +623,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
 
 template <int MODE, int MINB, int UNR, bool PROF = false>
 static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
-    auto kern = anneal_kernel<MODE, MINB, UNR, PROF>;
+    auto kern = a.n_ec == 1 ? anneal_kernel<MODE, MINB, UNR, PROF, true> : anneal_kernel<MODE, MINB, UNR, PROF, false>;
     const size_t smem = sizeof(AnnealSmem) + sizeof(RemEnt) * (size_t)(a.E * (a.E + 1) / 2);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

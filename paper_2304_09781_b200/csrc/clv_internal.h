@@ -128,6 +128,7 @@ struct AnnealArgs {
     FeasView F;
     const EvalConst *ec;
     int n_ec;
+    EvalConst ec0;                  // = ec[0] when n_ec == 1 (kernel-parameter copy)
     double t_init, cooling, t_floor;
     int stall_limit, max_steps, proposal, evaluate;
     int n, n_chains, E;
