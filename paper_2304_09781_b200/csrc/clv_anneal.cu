@@ -43,12 +43,12 @@ struct __align__(16) ARow {
 };
 
 struct __align__(8) RemEnt {            // one removal multiset R (single edge or pair), 56 B
-    double d0, d1, d2, d3;                 // -(rows of R), exact integers
+    double b0, b1, b2, b3;                 // centre aggregates minus the rows of R (exact integers)
     int pre;                               // doubles: exclusive prefix of move-list lengths
-    int off;                               // doubles: first entry of the static move list
-    unsigned short p;                      // pair index P(r1, r2) (doubles) / edge (singles)
+    int end;                               // doubles: pre + move-list length
+    int offm;                              // doubles: first static move-list entry minus pre
+    int ibase;                             // canonical index base: E*E + P(r1,r2)*NP (doubles), r*E (singles)
     unsigned short code;                   // slice code of R: sr1*125 + sr2*25 (doubles), sr*5 (singles)
-    unsigned char len;                     // doubles: move-list length
     unsigned char r1, r2;                  // removed edges (r2 = 0xFF for singles)
     unsigned char top;                     // latency rank of the top edge still present, NO_TOP if none
 };
@@ -240,10 +240,10 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
         const bool ok = (x == y) ? (s.w[x] >= 2) : (s.w[x] > 0 && s.w[y] > 0);
         if (!ok) continue;
         RemEnt &r = rp[pos++];
-        r.d0 = -(s.row[x].thr + s.row[y].thr);
-        r.d1 = -(s.row[x].acc + s.row[y].acc);
-        r.d2 = -(s.row[x].en + s.row[y].en);
-        r.d3 = -(s.row[x].idle + s.row[y].idle);
+        r.b0 = s.S[0] + -(s.row[x].thr + s.row[y].thr);
+        r.b1 = s.S[1] + -(s.row[x].acc + s.row[y].acc);
+        r.b2 = s.S[2] + -(s.row[x].en + s.row[y].en);
+        r.b3 = s.S[3] + -(s.row[x].idle + s.row[y].idle);
         unsigned long long m = s.pmask;
         if (x == y) { if (s.w[x] == 2) m &= ~s.rbit[x]; }
         else {
@@ -251,11 +251,11 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             if (s.w[y] == 1) m &= ~s.rbit[y];
         }
         r.top = top_rank(m);
-        r.p = (unsigned short)p;
-        r.off = s.pair_off[p];
-        r.len = s.pair_len[p];
+        r.ibase = E * E + p * NP;
         r.pre = lpos;
-        lpos += r.len;
+        r.offm = s.pair_off[p] - lpos;
+        lpos += s.pair_len[p];
+        r.end = lpos;
         r.code = (unsigned short)(s.sl[x] * 125 + s.sl[y] * 25);
         r.r1 = (unsigned char)x; r.r2 = (unsigned char)y;
     }
@@ -267,11 +267,12 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
             if (ok) {
                 RemEnt &r = s.se[c + __popc(bal & ((1u << lane) - 1u))];
-                r.d0 = -s.row[e].thr; r.d1 = -s.row[e].acc; r.d2 = -s.row[e].en; r.d3 = -s.row[e].idle;
+                r.b0 = s.S[0] + -s.row[e].thr; r.b1 = s.S[1] + -s.row[e].acc;
+                r.b2 = s.S[2] + -s.row[e].en; r.b3 = s.S[3] + -s.row[e].idle;
                 r.top = top_rank((s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask);
-                r.p = (unsigned short)e;
+                r.ibase = e * E;
                 r.code = (unsigned short)(s.sl[e] * 5);
-                r.r1 = (unsigned char)e; r.r2 = 0xFF; r.off = 0; r.len = 0; r.pre = 0;
+                r.r1 = (unsigned char)e; r.r2 = 0xFF; r.offm = 0; r.end = 0; r.pre = 0;
             }
             c += __popc(bal);
         }
@@ -406,7 +407,6 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     const int G = CL * ANT;
     const int gt = crank * ANT + tid;
     const unsigned long long mem_ok = s.mem_ok;
-    const int NPc = E * (E + 1) / 2;
 
     for (int k = 0; !done; ++k) {
         PROF_MARK(0);
@@ -424,8 +424,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (a != R.r1 && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]]) {
                     ++cnt;
                     const ARow &A = s.row[a];
-                    fold<MODE, EC1>(s, args, s.S[0] + R.d0 + A.thr, s.S[1] + R.d1 + A.acc, s.S[2] + R.d2 + A.en,
-                               s.S[3] + R.d3 + A.idle, dmax(s.lat_by_rank[R.top], s.lat_e[a]), (int)R.p * E + a,
+                    fold<MODE, EC1>(s, args, R.b0 + A.thr, R.b1 + A.acc, R.b2 + A.en,
+                               R.b3 + A.idle, dmax(s.lat_by_rank[R.top], s.lat_e[a]), R.ibase + a,
                                rS, rV, rP, args.seed, gchain, (uint64_t)k);
                 }
                 i += dI; a += dA;
@@ -455,17 +455,17 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                     for (int u = 0; u < UNR; ++u) {
                         const int tu = t + 32 * u;
                         if (tu < tend) {
-                            while (tu >= rp[j].pre + rp[j].len) ++j;
+                            while (tu >= rp[j].end) ++j;
                             const RemEnt &R = rp[j];
-                            const uint32_t ent = __ldg(plist + R.off + (tu - R.pre));
+                            const uint32_t ent = __ldg(plist + R.offm + tu);
                             if (s.feasD[R.code + ((ent >> 12) & 31)]) {
                                 ++cnt;
                                 const int a1 = ent & 63, a2 = (ent >> 6) & 63;
                                 const ARow &A1 = s.row[a1], &A2 = s.row[a2];
-                                fold<MODE, EC1>(s, args, s.S[0] + R.d0 + A1.thr + A2.thr, s.S[1] + R.d1 + A1.acc + A2.acc,
-                                           s.S[2] + R.d2 + A1.en + A2.en, s.S[3] + R.d3 + A1.idle + A2.idle,
+                                fold<MODE, EC1>(s, args, R.b0 + A1.thr + A2.thr, R.b1 + A1.acc + A2.acc,
+                                           R.b2 + A1.en + A2.en, R.b3 + A1.idle + A2.idle,
                                            dmax(s.lat_by_rank[R.top], dmax(s.lat_e[a1], s.lat_e[a2])),
-                                           E * E + (int)R.p * NPc + (int)(ent >> 17), rS, rV, rP, args.seed,
+                                           R.ibase + (int)(ent >> 17), rS, rV, rP, args.seed,
                                            gchain, (uint64_t)k);
                             }
                         }
