@@ -416,6 +416,8 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches_per_step * args.steps, "roofline": roof, "cpu_baseline": cpu,
             "replan_tts_ms": 1000.0 * dev_time / args.steps,
+            "replan_tts_cpu_s": (None if cpu is None else (evals_all / args.steps) / cpu["value"]),
+            "replan_tts_cpu_note": "candidates per re-plan / measured 1-core oracle rate (same chains, same algorithm)",
             "chain_steps_per_replan": chain_steps_all / args.steps,
             "wall_s_timed_region": t_wall}
     print(json.dumps(line), flush=True)
