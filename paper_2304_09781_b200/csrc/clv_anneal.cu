@@ -78,6 +78,20 @@ __device__ __forceinline__ KRec krec_min_warp(KRec r) {
     return r;
 }
 
+// (key, idx) minimum over the warp without payload: three redux.sync steps
+// (key high word, key low word, index) instead of five 3-shuffle rounds.
+__device__ __forceinline__ KRec krec_min_redux(KRec r) {
+    const unsigned hi = (unsigned)(r.key >> 32), lo = (unsigned)r.key;
+    const unsigned mh = __reduce_min_sync(0xFFFFFFFFu, hi);
+    const unsigned ml = __reduce_min_sync(0xFFFFFFFFu, hi == mh ? lo : 0xFFFFFFFFu);
+    const unsigned mi = __reduce_min_sync(0xFFFFFFFFu, (hi == mh && lo == ml) ? (unsigned)r.idx : 0xFFFFFFFFu);
+    KRec o;
+    o.key = ((unsigned long long)mh << 32) | ml;
+    o.idx = (int)mi;
+    o.hv = 0.0;
+    return o;
+}
+
 struct __align__(16) AnnealSmem {
     ARow row[CLV_MAX_EDGES];
     double lat_e[CLV_MAX_EDGES];           // p95 latency per edge
@@ -146,6 +160,16 @@ __device__ inline Score score_move(const AnnealSmem &s, int r1, int r2, int a1, 
         m |= s.rbit[f[k]];
     }
     return epilogue_d(t, ac, en, id, lmax_of(s, m), s.ec);
+}
+
+// Apply a move to a bare weight vector (best-graph reconstruction).
+__device__ inline void move_graph(const AnnealSmem &s, int E, long long idx, int *w) {
+    int r1, r2, a1, a2;
+    decode_move(s, E, idx, r1, r2, a1, a2);
+    if (r1 != 0xFF) w[r1] -= 1;
+    if (r2 != 0xFF) w[r2] -= 1;
+    if (a1 != 0xFF) w[a1] += 1;
+    if (a2 != 0xFF) w[a2] += 1;
 }
 
 // Apply a move to the CTA-local centre (thread 0) -- O(1).
@@ -477,10 +501,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         // ---- CTA reduction, then DSMEM broadcast of the CTA's records to every CTA
         {
             const int lane = tid & 31, wid = tid >> 5;
-            if (MODE != MODE_UNIFORM_PROPOSAL) { rS = krec_min_warp<false>(rS); rV = krec_min_warp<false>(rV); }
+            if (MODE != MODE_UNIFORM_PROPOSAL) { rS = krec_min_redux(rS); rV = krec_min_redux(rV); }
             if (MODE != MODE_BEST_ALL) rP = krec_min_warp<MODE == MODE_UNIFORM_ALL>(rP);
-#pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, m);
+            cnt = __reduce_add_sync(0xFFFFFFFFu, (unsigned)cnt);
             if (lane == 0) { s.wS[wid] = rS; s.wV[wid] = rV; s.wP[wid] = rP; s.wc[wid] = cnt; }
             __syncthreads();
             if (wid == 0) {
@@ -488,10 +511,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 rV = lane < NWARP ? s.wV[lane] : krec_none();
                 rP = lane < NWARP ? s.wP[lane] : krec_none();
                 cnt = lane < NWARP ? s.wc[lane] : 0ULL;
-                if (MODE != MODE_UNIFORM_PROPOSAL) { rS = krec_min_warp<false>(rS); rV = krec_min_warp<false>(rV); }
+                if (MODE != MODE_UNIFORM_PROPOSAL) { rS = krec_min_redux(rS); rV = krec_min_redux(rV); }
                 if (MODE != MODE_BEST_ALL) rP = krec_min_warp<MODE == MODE_UNIFORM_ALL>(rP);
-#pragma unroll
-                for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, m);
+                cnt = __reduce_add_sync(0xFFFFFFFFu, (unsigned)cnt);
                 // (after the xor butterflies every lane holds the CTA result)
                 if (lane < CL) {
                     AnnealSmem *ls = cluster.map_shared_rank(&s, lane);
@@ -555,17 +577,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                     }
                 }
                 const bool nb = (ck1 < bk1) || (ck1 == bk1 && ck2 < bk2);
-                if (nb) {
+                if (nb) {                          // the best graph is rebuilt at the end (move log)
                     bk1 = ck1; bk2 = ck2; best_step = k; best_idx = cidx; stall = 0;
-                    if (leader) {
-                        int c1, c2, c3, c4;
-                        decode_move(s, E, cidx, c1, c2, c3, c4);
-                        for (int e = 0; e < E; ++e) s.bw[e] = s.w[e];
-                        if (c1 != 0xFF) s.bw[c1] -= 1;
-                        if (c2 != 0xFF) s.bw[c2] -= 1;
-                        if (c3 != 0xFF) s.bw[c3] += 1;
-                        if (c4 != 0xFF) s.bw[c4] += 1;
-                    }
                 } else {
                     stall += 1;
                 }
@@ -581,6 +594,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                     args.log[(size_t)chain * args.max_steps + k] = row;
                 }
                 if (acc) { hc = hp; mv = pidx; }
+                if (leader) args.mvlog[(size_t)chain * args.max_steps + k] = (int)mv;
                 steps = k + 1;
                 if (stall >= args.stall_limit) { status = 1; fin = 1; }
             }
@@ -600,6 +614,16 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         for (int q = 0; q < 7; ++q) args.prof[((size_t)blockIdx.x) * 8 + q] = prof_acc[q];
 
     if (leader) {
+        // best graph = start + the accepted moves of steps < best_step + the best candidate's move
+        {
+            const uint16_t *w0 = args.start_w + (size_t)chain * E;
+            for (int e = 0; e < E; ++e) s.bw[e] = w0[e];
+            for (int kk = 0; kk < best_step; ++kk) {
+                const int m = args.mvlog[(size_t)chain * args.max_steps + kk];
+                if (m >= 0) move_graph(s, E, m, s.bw);
+            }
+            if (best_step >= 0) move_graph(s, E, best_idx, s.bw);
+        }
         clv_chain_result r;
         uint16_t *bw_out = args.best_w + (size_t)chain * E;
         uint16_t *fw_out = args.final_w + (size_t)chain * E;

@@ -171,6 +171,7 @@ void clv_destroy(clv_ctx *ctx) {
     cudaFree(ctx->ec_dev); cudaFree(ctx->small_dev);
     for (int f = 0; f < CLV_MAX_FAMILIES; ++f) cudaFree(ctx->pair_list_dev[f]);
     clv::sim_destroy(ctx->sim);
+    cudaFree(ctx->mvlog);
     delete ctx;
 }
 
@@ -554,6 +555,16 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
     a.stall_limit = ap->stall_limit; a.max_steps = ap->max_steps; a.proposal = ap->proposal; a.evaluate = ap->evaluate;
     a.n = n; a.n_chains = n_chains; a.E = ctx->fam[family].E; a.chain_base = chain_base; a.seed = seed;
     a.start_w = start_w_dev; a.res = results_dev; a.best_w = best_w_dev; a.final_w = final_w_dev; a.log = log_dev;
+    {
+        const size_t need = (size_t)n_chains * (size_t)std::max(ap->max_steps, 1);
+        if (need > ctx->mvlog_cap) {
+            cudaFree(ctx->mvlog);
+            ctx->mvlog = nullptr; ctx->mvlog_cap = 0;
+            CLV_CUDA(cudaMalloc(&ctx->mvlog, need * sizeof(int)), "alloc move log");
+            ctx->mvlog_cap = need;
+        }
+        a.mvlog = ctx->mvlog;
+    }
     {
         // debug phase profile buffer (CLV_ANNEAL_VARIANT=9 only)
         const char *v = getenv("CLV_ANNEAL_VARIANT");

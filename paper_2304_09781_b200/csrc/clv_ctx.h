@@ -45,4 +45,6 @@ struct clv_ctx {
     int ec_cap = 0;
     int32_t *small_dev = nullptr;             // realize scratch
     clv::SimState *sim = nullptr;             // serving simulator (clv_sim.cu)
+    int *mvlog = nullptr;                     // chain move logs (best-graph reconstruction)
+    size_t mvlog_cap = 0;
 };

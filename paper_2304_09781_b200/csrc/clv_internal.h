@@ -139,6 +139,7 @@ struct AnnealArgs {
     uint16_t *best_w;
     uint16_t *final_w;
     clv_log_row *log;
+    int *mvlog;                     // [n_chains][max_steps] accepted move per step (-1 = none)
     long long *prof;                // optional phase profile (debug variant only)
 };
 
