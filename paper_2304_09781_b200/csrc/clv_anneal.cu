@@ -350,7 +350,7 @@ __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : 
 
 template <int MODE, int MINB, int UNR, bool PROF = false, bool EC1 = false>
 __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
-    long long prof_acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long prof_last = 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     AnnealSmem &s = *reinterpret_cast<AnnealSmem *>(smem_raw);
@@ -434,7 +434,14 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
 
     for (int k = 0; !done; ++k) {
         PROF_MARK(0);
+        bool refreshed = false;
+        if (PROF) {
+#pragma unroll
+            for (int q = 0; q < CLV_K; ++q) refreshed |= (s.svec[q] != s.fsvec[q]);
+        }
+        const long long prep0 = PROF ? clock64() : 0;
         prepare_step(s, rp, E, n, args.F);
+        if (PROF && threadIdx.x == 0 && refreshed) prof_acc[7] += clock64() - prep0;
         PROF_MARK(1);
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
         unsigned long long cnt = 0;
@@ -611,7 +618,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     // Keep every CTA's shared memory alive until no peer can touch it over DSMEM.
     cluster.sync();
     if (PROF && threadIdx.x == 0 && args.prof)
-        for (int q = 0; q < 7; ++q) args.prof[((size_t)blockIdx.x) * 8 + q] = prof_acc[q];
+        for (int q = 0; q < 8; ++q) args.prof[((size_t)blockIdx.x) * 8 + q] = prof_acc[q];
 
     if (leader) {
         // best graph = start + the accepted moves of steps < best_step + the best candidate's move

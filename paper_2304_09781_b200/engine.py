@@ -122,6 +122,18 @@ class CloverEngine:
     def _check(self, rc: int) -> None:
         N.check(rc, self.ctx)
 
+    def staging(self, name: str, nbytes: int, pinned: bool = False):
+        """Grow-only cached byte buffer (device, or pinned host) for host-facing calls."""
+        torch = self.torch
+        cache = self.__dict__.setdefault("_staging", {})
+        buf = cache.get(name)
+        if buf is None or buf.numel() < nbytes:
+            size = max(int(nbytes), 256)
+            buf = (torch.empty(size, dtype=torch.uint8, pin_memory=True) if pinned
+                   else torch.empty(size, dtype=torch.uint8, device="cuda:%d" % self.device))
+            cache[name] = buf
+        return buf
+
     def _stream(self, stream=None) -> int:
         s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
         return s.cuda_stream

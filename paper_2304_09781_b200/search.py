@@ -17,7 +17,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from .core import ObjectiveParams, SliceType, derive_seed
-from .engine import CloverEngine, CHAIN_DTYPE, RECORD_DTYPE
+from .engine import AnnealBatch, CloverEngine, CHAIN_DTYPE, LOG_DTYPE, RECORD_DTYPE
 from .errors import CarbonSchedError, InfeasibleGraphError, NoNeighborError
 from .graph import ConfigGraph, build_graph
 from .mig import FleetConfig
@@ -138,22 +138,52 @@ def anneal_chains(engine: CloverEngine, starts, profile: ProfileTable, scenarios
     torch = engine.torch
     if isinstance(starts, (list, tuple)) and starts and isinstance(starts[0], ConfigGraph):
         starts = np.array([g.weights for g in starts], dtype=np.uint16)
-    host = torch.from_numpy(np.ascontiguousarray(np.asarray(starts, dtype=np.uint16)).view(np.int16))
-    host = host.pin_memory() if not host.is_pinned() else host
-    dev = host.to(device="cuda:%d" % engine.device, non_blocking=True).view(torch.uint16)
-    batch = engine.anneal(dev, profile, scenarios, ap, seed, chain_base=chain_base, cluster=cluster, log=log)
-    rec = engine.select_chains(batch)
+    starts = np.ascontiguousarray(np.asarray(starts, dtype=np.uint16))
+    n_chains, E = starts.shape
+    # H2D: cached pinned staging buffer -> cached device buffer (one async copy)
+    nb_in = starts.nbytes
+    h_in = engine.staging("ac_in_host", nb_in, pinned=True)
+    h_in.numpy()[:nb_in] = starts.view(np.uint8).reshape(-1)
+    d_in = engine.staging("ac_in_dev", nb_in)
+    d_in[:nb_in].copy_(h_in[:nb_in], non_blocking=True)
+    dev = d_in[:nb_in].view(torch.uint16).view(n_chains, E)
+    # outputs: one device buffer [results | best_w | final_w | record], one D2H copy
+    r_b = n_chains * CHAIN_DTYPE.itemsize
+    w_b = (n_chains * E * 2 + 15) // 16 * 16
+    total = r_b + 2 * w_b + 32
+    d_out = engine.staging("ac_out_dev", total)
+    steps = ap.step_limit()
+    batch = AnnealBatch(d_out[:r_b], d_out[r_b:r_b + n_chains * E * 2].view(torch.uint16).view(n_chains, E),
+                        d_out[r_b + w_b:r_b + w_b + n_chains * E * 2].view(torch.uint16).view(n_chains, E),
+                        torch.zeros(max(1, n_chains * steps * 56), dtype=torch.uint8, device=d_out.device)
+                        if log else None, n_chains, chain_base, steps)
+    batch = engine.anneal(dev, profile, scenarios, ap, seed, chain_base=chain_base, cluster=cluster, log=log,
+                          out=batch)
+    rec_dev = d_out[r_b + 2 * w_b:total]
+    rec = engine.select_chains(batch, record=rec_dev)
     if exchange:
         rec = exchange_record(engine, rec, group)
-    out = batch.host()
-    record = np.frombuffer(rec.cpu().numpy().tobytes(), dtype=RECORD_DTYPE)[0]
-    res = out["results"]
+        if rec.data_ptr() != rec_dev.data_ptr():
+            rec_dev.copy_(rec)
+    h_out = engine.staging("ac_out_host", total, pinned=True)
+    h_out[:total].copy_(d_out[:total], non_blocking=True)
+    log_host = batch.log.cpu() if log else None          # (synchronises; log is a debug output)
+    torch.cuda.current_stream(engine.device).synchronize()
+    raw = h_out.numpy()[:total].copy()
+    res = np.frombuffer(raw[:r_b].tobytes(), dtype=CHAIN_DTYPE)
+    best_w = raw[r_b:r_b + n_chains * E * 2].view(np.uint16).reshape(n_chains, E)
+    final_w = raw[r_b + w_b:r_b + w_b + n_chains * E * 2].view(np.uint16).reshape(n_chains, E)
+    record = np.frombuffer(raw[r_b + 2 * w_b:total].tobytes(), dtype=RECORD_DTYPE)[0]
+    log_arr = None
+    if log_host is not None:
+        log_arr = np.frombuffer(log_host.numpy().tobytes(), dtype=LOG_DTYPE)[:n_chains * steps].reshape(
+            n_chains, steps)
     local = int(record["index"]) - chain_base
     if not 0 <= local < len(res):        # the winner lives on another rank: report ours
         local = int(np.lexsort((np.arange(len(res)), res["h"], res["sla_met"] == 0))[0])
-    g = ConfigGraph(out["best_w"][local].astype(np.int64), profile.variant_count, profile.name)
-    return ChainsResult(_result_from_chain(res[local], g), chain_base + local, res, out["best_w"],
-                        out["final_w"], int(res["evals"].sum()), record, out.get("log"))
+    g = ConfigGraph(best_w[local].astype(np.int64), profile.variant_count, profile.name)
+    return ChainsResult(_result_from_chain(res[local], g), chain_base + local, res, best_w,
+                        final_w, int(res["evals"].sum()), record, log_arr)
 
 
 def anneal(start: ConfigGraph, n: int, profile: ProfileTable, workload: Workload, ci: float,

@@ -18,5 +18,6 @@ for cl in (3,):
     buf=buf.reshape(len(st),cl,8)
     names=["prepare","score","cta_reduce","sync1","leader","sync2","apply"]
     lead=buf[:,0,:7].mean(0)/64; other=buf[:,1,:7].mean(0)/64
+    print("prepare cycles spent in steps that refreshed the slice-delta feasibility (per step avg):", int(buf[:,0,7].mean()/64))
     print("cluster",cl,"cycles/step leader:", {k:int(v) for k,v in zip(names,lead)}, "\n  rank1:", {k:int(v) for k,v in zip(names,other)})
 
