@@ -206,34 +206,53 @@ __device__ __forceinline__ unsigned char top_rank(unsigned long long m) {
 __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, int n, const FeasView &F) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int NP = E * (E + 1) / 2;
-    const int PER = (NP + ANT - 1) / ANT;          // consecutive pairs per thread (<= 4)
+    constexpr int PER = (MAXP + ANT - 1) / ANT;    // consecutive pairs per thread (4 at E <= 40)
+    static_assert(PER == 4, "pair split assumes <= 1024 removal pairs");
     bool refresh = false;
 #pragma unroll
     for (int k = 0; k < CLV_K; ++k) refresh |= (s.svec[k] != s.fsvec[k]);
+    // Feasibility of the 650 slice deltas, 3 per thread, as two batched round trips:
+    // all rectangle offsets first, then all bitset words (feasible() in clv_common.cuh
+    // would serialise the 2 dependent loads of each lookup).
     bool fres[3] = {false, false, false};
     if (refresh) {                                 // uniform across the CTA
+        uint32_t obase[3], wofs[3], bit[3];
+        bool cand[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             const int t = threadIdx.x + q * ANT;
-            if (t >= 650) continue;
             int v[CLV_K];
 #pragma unroll
             for (int k = 0; k < CLV_K; ++k) v[k] = s.svec[k];
-            bool ok;
+            bool ok = t < 650;
             if (t < 25) {
                 v[t / 5] -= 1; v[t % 5] += 1;
-                ok = v[t / 5] >= 0;
-            } else {
+            } else if (t < 650) {
                 const int u = t - 25;
                 v[u / 125] -= 1; v[(u / 25) % 5] -= 1; v[(u / 5) % 5] += 1; v[u % 5] += 1;
-                ok = v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[3] >= 0 && v[4] >= 0;
             }
-            fres[q] = ok && feasible(F, n, v[0], v[1], v[2], v[3], v[4]);
+            ok = ok && v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[3] >= 0 && v[4] >= 0;
+            // feasible(F, n, v...) split into its index arithmetic and its two loads
+            ok = ok && v[0] <= n && (v[0] == 0 || F.has7g);
+            const int N = n - v[0];
+            const int R = 7 * N - 4 * v[1] - 3 * v[2];
+            ok = ok && N <= F.nmax && R >= 0 && R - 2 * v[3] >= 0 && v[4] <= R - 2 * v[3];
+            cand[q] = ok;
+            obase[q] = ok ? __ldg(F.off + ((size_t)N * F.bdim + v[1]) * F.cdim + v[2]) : 0u;
+            wofs[q] = ok ? (uint32_t)v[3] * (uint32_t)((R + 32) >> 5) + (uint32_t)(v[4] >> 5) : 0u;
+            bit[q] = (uint32_t)(v[4] & 31);
         }
+        uint32_t word[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) word[q] = cand[q] ? __ldg(F.bits + obase[q] + wofs[q]) : 0u;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) fres[q] = cand[q] && ((word[q] >> bit[q]) & 1u);
     }
     const int p0 = threadIdx.x * PER;
     int cnt = 0, lsum = 0;
-    for (int p = p0; p < p0 + PER && p < NP; ++p) {
+#pragma unroll
+    for (int p = p0; p < p0 + PER; ++p) {
+        if (p >= NP) break;
         const int x = s.pair_tab[p] & 0xFF, y = s.pair_tab[p] >> 8;
         const bool ok = (x == y) ? (s.w[x] >= 2) : (s.w[x] > 0 && s.w[y] > 0);
         if (ok) { ++cnt; lsum += s.pair_len[p]; }
@@ -259,7 +278,9 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
     }
     __syncthreads();
     int pos = s.warp_off[wid] + ic - cnt, lpos = s.warp_len[wid] + il - lsum;
-    for (int p = p0; p < p0 + PER && p < NP; ++p) {
+#pragma unroll 1
+    for (int p = p0; p < p0 + PER; ++p) {
+        if (p >= NP) break;
         const int x = s.pair_tab[p] & 0xFF, y = s.pair_tab[p] >> 8;
         const bool ok = (x == y) ? (s.w[x] >= 2) : (s.w[x] > 0 && s.w[y] > 0);
         if (!ok) continue;
@@ -283,7 +304,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
         r.code = (unsigned short)(s.sl[x] * 125 + s.sl[y] * 25);
         r.r1 = (unsigned char)x; r.r2 = (unsigned char)y;
     }
-    if (wid == 0) {
+    if (wid == NWARP - 1) {                        // warp 0 runs the second-level scan above
         int c = 0;
         for (int e0 = 0; e0 < E; e0 += 32) {
             const int e = e0 + lane;
@@ -441,7 +462,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         }
         const long long prep0 = PROF ? clock64() : 0;
         prepare_step(s, rp, E, n, args.F);
-        if (PROF && threadIdx.x == 0 && refreshed) prof_acc[7] += clock64() - prep0;
+        if (PROF && threadIdx.x == 0 && refreshed) { prof_acc[7] += clock64() - prep0; prof_acc[6] -= 1000000; }
         PROF_MARK(1);
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
         unsigned long long cnt = 0;
@@ -591,8 +612,11 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 }
                 const double T0 = args.t_init - (double)k * args.cooling;
                 const double Tk = args.t_floor >= T0 ? args.t_floor : T0;
-                const double u = uniform01(derive_seed4(args.seed, gchain, (uint64_t)k, 0ULL));
-                const bool acc = (hp <= hc) || (u < exp_clv(-(hp - hc) / Tk));
+                bool acc = hp <= hc;                 // Eq. 7: the draw only matters for worse moves
+                if (!acc) {
+                    const double u = uniform01(derive_seed4(args.seed, gchain, (uint64_t)k, 0ULL));
+                    acc = u < exp_clv(-(hp - hc) / Tk);
+                }
                 if (args.log && leader) {
                     clv_log_row row;
                     row.temp = Tk; row.f = fp; row.h = hp; row.p95_ms = Lp;

@@ -139,12 +139,23 @@ class CloverEngine:
         return s.cuda_stream
 
     # -- tables ----------------------------------------------------------------
-    def add_profile(self, profile: ProfileTable) -> int:
-        if profile.name in self._families:
-            return self._families[profile.name][0]
-        fam = len(self._families)
-        if fam >= 8:
-            raise CarbonSchedError("at most 8 profile families per engine")
+    def add_profile(self, profile: ProfileTable, pinned: Sequence[str] = ()) -> int:
+        """Device family slot of ``profile`` (tables uploaded on first use).  The 8 slots are
+        recycled least-recently-used; ``pinned`` keys (profiles of the same call) are kept."""
+        key = self._profile_key(profile)
+        lru = self.__dict__.setdefault("_lru", [])
+        if key in self._families:
+            lru.remove(key)
+            lru.append(key)
+            return self._families[key][0]
+        if len(self._families) < 8:
+            fam = len(self._families)
+        else:
+            victim = next((k for k in lru if k not in pinned), None)
+            if victim is None:
+                raise CarbonSchedError("more than 8 profile families in one call")
+            fam = self._families.pop(victim)[0]
+            lru.remove(victim)
         if profile.topology is not self.topology and profile.topology.to_json_dict() != self.topology.to_json_dict():
             raise CarbonSchedError("profile was built for a different topology")
         t = profile.scoring_tables()
@@ -155,8 +166,23 @@ class CloverEngine:
                                              en.ctypes.data, idle.ctypes.data, lat.ctypes.data, mem.ctypes.data,
                                              t.kt, t.ke, t.ki))
         self._set_sim_profile(fam, profile)
-        self._families[profile.name] = (fam, profile, t)
+        self._families[key] = (fam, profile, t)
+        lru.append(key)
         return fam
+
+    @staticmethod
+    def _profile_key(profile: ProfileTable) -> str:
+        key = getattr(profile, "_engine_key", None)
+        if key is None:
+            import hashlib
+            import json
+            digest = hashlib.sha1(json.dumps(profile.to_json_dict(), sort_keys=True).encode()).hexdigest()[:16]
+            key = "%s#%s" % (profile.name, digest)
+            try:
+                object.__setattr__(profile, "_engine_key", key)
+            except Exception:
+                pass
+        return key
 
     def _set_sim_profile(self, fam: int, profile: ProfileTable) -> None:
         """Simulator rows of the family: per edge mean, distribution, sigma, energy."""
@@ -387,8 +413,9 @@ class CloverEngine:
     # -- counter-RNG sweep ------------------------------------------------------------
     def _pods(self, pods):
         arr = (N.Pod * len(pods))()
+        keys = [self._profile_key(p[0]) for p in pods]
         for i, (profile, scenario, n_gpus, weight) in enumerate(pods):
-            arr[i] = N.Pod(self.add_profile(profile), int(n_gpus), float(weight), eval_params(scenario))
+            arr[i] = N.Pod(self.add_profile(profile, pinned=keys), int(n_gpus), float(weight), eval_params(scenario))
         return arr
 
     def sweep(self, pods, begin: int, end: int, seed: int, outputs: bool = False, stream=None):

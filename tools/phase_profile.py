@@ -18,6 +18,10 @@ for cl in (3,):
     buf=buf.reshape(len(st),cl,8)
     names=["prepare","score","cta_reduce","sync1","leader","sync2","apply"]
     lead=buf[:,0,:7].mean(0)/64; other=buf[:,1,:7].mean(0)/64
-    print("prepare cycles spent in steps that refreshed the slice-delta feasibility (per step avg):", int(buf[:,0,7].mean()/64))
+    nref = -(buf[:,0,6] // 1000000)        # refresh steps are counted in the 'apply' slot (-1e6 each)
+    buf[:,:,6] = buf[:,:,6] % 1000000
+    print("refresh steps per chain (of 64):", float(nref.mean()), " prepare cycles per refresh step:",
+          int(buf[:,0,7].sum() / max(nref.sum(), 1)), " per other step:",
+          int((buf[:,0,0].sum() - buf[:,0,7].sum()) / max(64 * len(buf) - nref.sum(), 1)))
     print("cluster",cl,"cycles/step leader:", {k:int(v) for k,v in zip(names,lead)}, "\n  rank1:", {k:int(v) for k,v in zip(names,other)})
 
