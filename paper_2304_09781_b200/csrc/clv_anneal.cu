@@ -359,7 +359,8 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args
 }
 
 // Optional phase profiler (CLV_ANNEAL_VARIANT=9): thread 0 of each CTA accumulates
-// clock64 deltas between consecutive marks into args.prof[(chain*CL+rank)*8 + phase].
+// clock64 deltas between consecutive marks into args.prof[(chain*CL+rank)*PROF_SLOTS + phase];
+// slot 7 = prepare cycles of steps that refreshed the slice-delta feasibility, slot 8 = their count.
 #define PROF_MARK(ph)                                                                  \
     if (PROF && threadIdx.x == 0) {                                                    \
         const long long _now = clock64();                                              \
@@ -371,7 +372,7 @@ __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : 
 
 template <int MODE, int MINB, int UNR, bool PROF = false, bool EC1 = false>
 __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
-    long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long prof_acc[PROF_SLOTS] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long prof_last = 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     AnnealSmem &s = *reinterpret_cast<AnnealSmem *>(smem_raw);
@@ -462,7 +463,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         }
         const long long prep0 = PROF ? clock64() : 0;
         prepare_step(s, rp, E, n, args.F);
-        if (PROF && threadIdx.x == 0 && refreshed) { prof_acc[7] += clock64() - prep0; prof_acc[6] -= 1000000; }
+        if (PROF && threadIdx.x == 0 && refreshed) { prof_acc[7] += clock64() - prep0; prof_acc[8] += 1; }
         PROF_MARK(1);
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
         unsigned long long cnt = 0;
@@ -642,7 +643,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     // Keep every CTA's shared memory alive until no peer can touch it over DSMEM.
     cluster.sync();
     if (PROF && threadIdx.x == 0 && args.prof)
-        for (int q = 0; q < 8; ++q) args.prof[((size_t)blockIdx.x) * 8 + q] = prof_acc[q];
+        for (int q = 0; q < PROF_SLOTS; ++q) args.prof[((size_t)blockIdx.x) * PROF_SLOTS + q] = prof_acc[q];
 
     if (leader) {
         // best graph = start + the accepted moves of steps < best_step + the best candidate's move

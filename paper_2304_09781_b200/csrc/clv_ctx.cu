@@ -569,7 +569,7 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
         // debug phase profile buffer (CLV_ANNEAL_VARIANT=9 only)
         const char *v = getenv("CLV_ANNEAL_VARIANT");
         if (v && atoi(v) == 9) {
-            size_t need = (size_t)n_chains * 16 * 8;
+            size_t need = (size_t)n_chains * 16 * PROF_SLOTS;
             if (prof_cap < need) { cudaFree(prof_buf); cudaMalloc(&prof_buf, need * sizeof(long long)); prof_cap = need; }
             cudaMemsetAsync(prof_buf, 0, need * sizeof(long long), st);
             a.prof = prof_buf;

@@ -1,27 +1,47 @@
-"""Per-phase cycle profile of the chain kernel (CLV_ANNEAL_VARIANT=9 build variant): cycles per step by phase."""
-import sys; sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
-import numpy as np, torch, time, ctypes, os
-from paper_2304_09781_b200.engine import CloverEngine
-from paper_2304_09781_b200.profiles import synthetic_profile
-from paper_2304_09781_b200.objective import AnnealParams
-from paper_2304_09781_b200 import _native as N
-import bench
-eng=CloverEngine(n_max=64); prof=synthetic_profile('efficientnet')
-sc=eng.calibrate(prof,64,350.0,0.5)
-st=bench.make_starts(eng,prof,bench.SEED,0,128)
-ap=AnnealParams(max_steps=64)
-lib=N.load(); lib.clv_debug_anneal_profile.argtypes=[ctypes.c_void_p, ctypes.c_size_t]
-for cl in (3,):
-    b=eng.anneal(st,prof,sc,ap,1,cluster=cl); torch.cuda.synchronize()
-    nb=len(st)*cl
-    buf=np.zeros(nb*8,dtype=np.int64); lib.clv_debug_anneal_profile(buf.ctypes.data, nb*8)
-    buf=buf.reshape(len(st),cl,8)
-    names=["prepare","score","cta_reduce","sync1","leader","sync2","apply"]
-    lead=buf[:,0,:7].mean(0)/64; other=buf[:,1,:7].mean(0)/64
-    nref = -(buf[:,0,6] // 1000000)        # refresh steps are counted in the 'apply' slot (-1e6 each)
-    buf[:,:,6] = buf[:,:,6] % 1000000
-    print("refresh steps per chain (of 64):", float(nref.mean()), " prepare cycles per refresh step:",
-          int(buf[:,0,7].sum() / max(nref.sum(), 1)), " per other step:",
-          int((buf[:,0,0].sum() - buf[:,0,7].sum()) / max(64 * len(buf) - nref.sum(), 1)))
-    print("cluster",cl,"cycles/step leader:", {k:int(v) for k,v in zip(names,lead)}, "\n  rank1:", {k:int(v) for k,v in zip(names,other)})
+"""Per-phase cycle profile of the chain kernel (build variant CLV_ANNEAL_VARIANT=9).
 
+Prints the mean cycles per chain step of each phase for the leader CTA and one
+other CTA of the cluster, and how often the slice-delta feasibility refresh runs.
+Run on the GPU box:  CLV_ANNEAL_VARIANT=9 python tools/phase_profile.py
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+from paper_2304_09781_b200 import _native as N  # noqa: E402
+from paper_2304_09781_b200.engine import CloverEngine  # noqa: E402
+from paper_2304_09781_b200.objective import AnnealParams  # noqa: E402
+from paper_2304_09781_b200.profiles import synthetic_profile  # noqa: E402
+
+SLOTS = 10
+NAMES = ["prepare", "score", "cta_reduce", "sync1", "leader", "sync2", "apply"]
+
+eng = CloverEngine(n_max=64)
+prof = synthetic_profile("efficientnet")
+sc = eng.calibrate(prof, 64, 350.0, 0.5)
+st = bench.make_starts(eng, prof, bench.SEED, 0, 128)
+ap = AnnealParams(max_steps=64)
+lib = N.load()
+lib.clv_debug_anneal_profile.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+cl = 3
+b = eng.anneal(st, prof, sc, ap, 1, cluster=cl)
+torch.cuda.synchronize()
+steps = b.host()["results"]["steps"].astype(np.float64)
+nb = len(st) * cl
+buf = np.zeros(nb * SLOTS, dtype=np.int64)
+lib.clv_debug_anneal_profile(buf.ctypes.data, nb * SLOTS)
+buf = buf.reshape(len(st), cl, SLOTS)
+per_step = lambda x: x.sum() / steps.sum()
+lead = {k: int(per_step(buf[:, 0, q])) for q, k in enumerate(NAMES)}
+other = {k: int(per_step(buf[:, 1, q])) for q, k in enumerate(NAMES)}
+nref = buf[:, 0, 8].sum()
+print("cluster %d cycles/step leader CTA: %s\n  rank-1 CTA: %s" % (cl, lead, other))
+print("feasibility refresh in %.1f%% of steps; prepare cycles per refresh step %d, per other step %d"
+      % (100.0 * nref / steps.sum(), buf[:, 0, 7].sum() / max(nref, 1),
+         (buf[:, 0, 0].sum() - buf[:, 0, 7].sum()) / max(steps.sum() - nref, 1)))
