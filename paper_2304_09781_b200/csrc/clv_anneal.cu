@@ -99,6 +99,7 @@ struct __align__(16) AnnealSmem {
     unsigned long long rbit[CLV_MAX_EDGES];// 1 << latency rank
     EvalConst ec;
     unsigned long long mem_ok;
+    unsigned magicE, magicNP;              // ceil(2^32 / E), ceil(2^32 / NP) (exact small divisions)
     unsigned char sl[CLV_MAX_EDGES];       // slice kind of the edge
     unsigned short pair_tab[MAXP];         // P -> (x | y << 8)
     int pair_off[MAXP];                    // static move lists (staged from FamilyTables)
@@ -130,14 +131,15 @@ __device__ __forceinline__ double lmax_of(const AnnealSmem &s, unsigned long lon
 
 // canonical index -> move (r1, r2, a1, a2; 0xFF = absent); indices are < 2^31
 __device__ inline void decode_move(const AnnealSmem &s, int E, long long idx64, int &r1, int &r2, int &a1, int &a2) {
+    // divisions by E and NP as multiply-high by ceil(2^32 / d): exact because n * d < 2^32
     const unsigned idx = (unsigned)idx64;
     if (idx < (unsigned)(E * E)) {
-        r1 = (int)(idx / (unsigned)E); a1 = (int)(idx - (unsigned)r1 * E); r2 = 0xFF; a2 = 0xFF;
+        r1 = (int)__umulhi(idx, s.magicE); a1 = (int)(idx - (unsigned)r1 * E); r2 = 0xFF; a2 = 0xFF;
         return;
     }
     const unsigned NP = (unsigned)(E * (E + 1) / 2);
     const unsigned u = idx - (unsigned)(E * E);
-    const int p = (int)(u / NP), q = (int)(u - (unsigned)p * NP);
+    const int p = (int)__umulhi(u, s.magicNP), q = (int)(u - (unsigned)p * NP);
     r1 = s.pair_tab[p] & 0xFF; r2 = s.pair_tab[p] >> 8;
     a1 = s.pair_tab[q] & 0xFF; a2 = s.pair_tab[q] >> 8;
 }
@@ -174,24 +176,36 @@ __device__ inline void move_graph(const AnnealSmem &s, int E, long long idx, int
 
 // Apply a move to the CTA-local centre (thread 0) -- O(1).
 __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
-    int r[2], a[2];
-    decode_move(s, E, idx, r[0], r[1], a[0], a[1]);
-    for (int k = 0; k < 2; ++k) {
-        if (r[k] == 0xFF) continue;
-        const int e = r[k];
-        s.w[e] -= 1;
-        s.S[0] -= s.row[e].thr; s.S[1] -= s.row[e].acc; s.S[2] -= s.row[e].en; s.S[3] -= s.row[e].idle;
-        s.svec[s.sl[e]] -= 1;
-        if (s.w[e] == 0) s.pmask &= ~s.rbit[e];
-    }
-    for (int k = 0; k < 2; ++k) {
-        if (a[k] == 0xFF) continue;
-        const int e = a[k];
-        s.w[e] += 1;
-        s.S[0] += s.row[e].thr; s.S[1] += s.row[e].acc; s.S[2] += s.row[e].en; s.S[3] += s.row[e].idle;
-        s.svec[s.sl[e]] += 1;
-        s.pmask |= s.rbit[e];
-    }
+    // All loads first, one update per field: the centre sums are exact integers, so
+    // S + ((A1 + A2) - (R1 + R2)) equals the edge-by-edge update bit for bit.
+    int r1, r2, a1, a2;
+    decode_move(s, E, idx, r1, r2, a1, a2);
+    const bool two = r2 != 0xFF;                   // a double move has r2 and a2
+    const ARow R1 = s.row[r1], A1 = s.row[a1];
+    ARow R2 = {0.0, 0.0, 0.0, 0.0}, A2 = {0.0, 0.0, 0.0, 0.0};
+    int wr2 = 0, wa2 = 0;
+    if (two) { R2 = s.row[r2]; A2 = s.row[a2]; wr2 = s.w[r2]; wa2 = s.w[a2]; }
+    const int wr1 = s.w[r1], wa1 = s.w[a1];
+    unsigned long long m = s.pmask;
+    const unsigned long long br1 = s.rbit[r1], ba1 = s.rbit[a1];
+    const unsigned long long br2 = two ? s.rbit[r2] : 0ULL, ba2 = two ? s.rbit[a2] : 0ULL;
+    s.S[0] = s.S[0] + ((A1.thr + A2.thr) - (R1.thr + R2.thr));
+    s.S[1] = s.S[1] + ((A1.acc + A2.acc) - (R1.acc + R2.acc));
+    s.S[2] = s.S[2] + ((A1.en + A2.en) - (R1.en + R2.en));
+    s.S[3] = s.S[3] + ((A1.idle + A2.idle) - (R1.idle + R2.idle));
+    const int nr1 = wr1 - 1 - ((two && r2 == r1) ? 1 : 0);
+    const int nr2 = two ? ((r2 == r1) ? nr1 : wr2 - 1) : 1;
+    const int na1 = wa1 + 1 + ((two && a2 == a1) ? 1 : 0);
+    s.w[r1] = nr1;
+    s.w[a1] = na1;
+    if (two) { s.w[r2] = nr2; s.w[a2] = (a2 == a1) ? na1 : wa2 + 1; }
+    const int kr1 = r1 % CLV_K, ka1 = a1 % CLV_K, kr2 = two ? r2 % CLV_K : -1, ka2 = two ? a2 % CLV_K : -1;
+#pragma unroll
+    for (int k = 0; k < CLV_K; ++k)
+        s.svec[k] += (k == ka1) + (k == ka2) - (k == kr1) - (k == kr2);
+    if (nr1 == 0) m &= ~br1;
+    if (nr2 == 0) m &= ~br2;
+    s.pmask = m | ba1 | ba2;
 }
 
 __device__ __forceinline__ unsigned char top_rank(unsigned long long m) {
@@ -405,6 +419,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     if (tid == 0) {
         s.lat_by_rank[NO_TOP] = 0.0;
         s.mem_ok = T.mem_ok;
+        s.magicE = 0xFFFFFFFFu / (unsigned)E + 1u;
+        s.magicNP = 0xFFFFFFFFu / (unsigned)(E * (E + 1) / 2) + 1u;
         s.ec = args.ec[args.n_ec == 1 ? 0 : chain];
     }
     __syncthreads();
@@ -631,8 +647,10 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (stall >= args.stall_limit) { status = 1; fin = 1; }
             }
             if (!fin && k + 1 >= args.max_steps) { status = 0; fin = 1; }
+            const long long ap0 = PROF ? clock64() : 0;
             if (mv != NOIDX) apply_move(s, E, mv);
             s.dec_done = fin;
+            if (PROF) prof_acc[9] += clock64() - ap0;
         }
         PROF_MARK(5);
         __syncthreads();

@@ -42,6 +42,7 @@ lead = {k: int(per_step(buf[:, 0, q])) for q, k in enumerate(NAMES)}
 other = {k: int(per_step(buf[:, 1, q])) for q, k in enumerate(NAMES)}
 nref = buf[:, 0, 8].sum()
 print("cluster %d cycles/step leader CTA: %s\n  rank-1 CTA: %s" % (cl, lead, other))
+print("leader: apply_move %d cycles per step" % per_step(buf[:, 0, 9]))
 print("feasibility refresh in %.1f%% of steps; prepare cycles per refresh step %d, per other step %d"
       % (100.0 * nref / steps.sum(), buf[:, 0, 7].sum() / max(nref, 1),
          (buf[:, 0, 0].sum() - buf[:, 0, 7].sum()) / max(steps.sum() - nref, 1)))
