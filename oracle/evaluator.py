@@ -45,10 +45,11 @@ def aggregates(W: np.ndarray, tables: OracleTables):
     cnt = W.reshape(len(W), tables.V, 5).sum(axis=1)
     s_idle = cnt @ tables.idle_q
     lmax = np.where(W > 0, tables.lat95[None, :], -np.inf).max(axis=1)
-    return s_thr, s_acc, s_en, s_idle, lmax
+    m = W.sum(axis=1)
+    return s_thr, s_acc, s_en, s_idle, lmax, m
 
 
-def epilogue(s_thr, s_acc, s_en, s_idle, lmax, tables, scenario) -> Evaluated:
+def epilogue(s_thr, s_acc, s_en, s_idle, lmax, m, tables, scenario) -> Evaluated:
     c = constants(tables, scenario)
     obj = scenario.obj
     a_base, c_base, slo = obj.base_accuracy, obj.base_carbon_g, obj.latency_slo_ms
@@ -64,7 +65,13 @@ def epilogue(s_thr, s_acc, s_en, s_idle, lmax, tables, scenario) -> Evaluated:
         p_idle = s_idle.astype(np.float64) * c["idle_scale"]
         E = e_act + ((1.0 - rho_c) * p_idle) * c["inv_3600R"]
         rho_q = np.minimum(rho, scenario.rho_sat)
-        L = lmax / (1.0 - rho_q)
+        # many-server p95: L = Lmax * (1 + rho^8 / (m (1 - rho)))
+        q1 = 1.0 - rho_q
+        r2 = rho_q * rho_q
+        r4 = r2 * r2
+        r8 = r4 * r4
+        wq = r8 / (np.asarray(m, dtype=np.float64) * q1)
+        L = lmax * (1.0 + wq)
         dA = (A - a_base) * kA
         dC = 100.0 - E * kC
         f = lam * dC + (1.0 - lam) * dA

@@ -107,6 +107,7 @@ struct __align__(16) AnnealSmem {
     // centre
     int w[CLV_MAX_EDGES];
     double S[4];
+    double mcount;                         // instances of the chain (every GED move keeps it)
     int svec[CLV_K];
     unsigned long long pmask;              // presence by latency rank
     // per-step tables (the pair entries live in the dynamic tail)
@@ -161,7 +162,7 @@ __device__ inline Score score_move(const AnnealSmem &s, int r1, int r2, int a1, 
         t += s.row[f[k]].thr; ac += s.row[f[k]].acc; en += s.row[f[k]].en; id += s.row[f[k]].idle;
         m |= s.rbit[f[k]];
     }
-    return epilogue_d(t, ac, en, id, lmax_of(s, m), s.ec);
+    return epilogue_d(t, ac, en, id, lmax_of(s, m), s.mcount, s.ec);
 }
 
 // Apply a move to a bare weight vector (best-graph reconstruction).
@@ -351,8 +352,8 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
 // Exact score of one neighbour folded into the thread's records.
 template <int MODE, bool EC1>
 __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args, double t, double ac, double en,
-                                     double id, double lmax, int idx, KRec &rS, KRec &rV, KRec &rP, uint64_t seed,
-                                     uint64_t gchain, uint64_t k) {
+                                     double id, double lmax, double mcnt, int idx, KRec &rS, KRec &rV, KRec &rP,
+                                     uint64_t seed, uint64_t gchain, uint64_t k) {
     if (MODE == MODE_UNIFORM_PROPOSAL) {
         const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
         if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; }
@@ -361,8 +362,8 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args
     // one evaluation scenario for every chain: its constants are kernel parameters
     // (constant-bank operands); per-chain scenarios come from the CTA's shared copy
     Score sc;
-    if constexpr (EC1) sc = epilogue_d(t, ac, en, id, lmax, args.ec0);
-    else sc = epilogue_d(t, ac, en, id, lmax, s.ec);
+    if constexpr (EC1) sc = epilogue_d(t, ac, en, id, lmax, mcnt, args.ec0);
+    else sc = epilogue_d(t, ac, en, id, lmax, mcnt, s.ec);
     const unsigned long long key = okey(sc.h);
     if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; } }
     else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; } }
@@ -438,6 +439,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         }
         s.S[0] = S0; s.S[1] = S1; s.S[2] = S2; s.S[3] = S3;
         s.pmask = m;
+        int cnt = 0;
+        for (int e = 0; e < E; ++e) cnt += s.w[e];
+        s.mcount = (double)cnt;
     }
     __syncthreads();
 
@@ -457,7 +461,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         }
         if (tot < 1 || !feasible(args.F, n, s.svec[0], s.svec[1], s.svec[2], s.svec[3], s.svec[4])) invalid = 1;
         edge_evals = __popcll(s.pmask);
-        const Score sc = epilogue_d(s.S[0], s.S[1], s.S[2], s.S[3], lmax_of(s, s.pmask), s.ec);
+        const Score sc = epilogue_d(s.S[0], s.S[1], s.S[2], s.S[3], lmax_of(s, s.pmask), s.mcount, s.ec);
         hc = sc.h;
         bk1 = sc.sla ? 0u : 1u; bk2 = okey(sc.h);
         for (int e = 0; e < E; ++e) s.bw[e] = s.w[e];
@@ -466,6 +470,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     }
     cluster.sync();                          // all CTAs started before any DSMEM traffic
     bool done = s.dec_done;
+    const double mcnt = s.mcount;
     const int G = CL * ANT;
     const int gt = crank * ANT + tid;
     const unsigned long long mem_ok = s.mem_ok;
@@ -494,7 +499,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                     ++cnt;
                     const ARow &A = s.row[a];
                     fold<MODE, EC1>(s, args, R.b0 + A.thr, R.b1 + A.acc, R.b2 + A.en,
-                               R.b3 + A.idle, dmax(s.lat_by_rank[R.top], s.lat_e[a]), R.ibase + a,
+                               R.b3 + A.idle, dmax(s.lat_by_rank[R.top], s.lat_e[a]), mcnt, R.ibase + a,
                                rS, rV, rP, args.seed, gchain, (uint64_t)k);
                 }
                 i += dI; a += dA;
@@ -533,7 +538,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                                 const ARow &A1 = s.row[a1], &A2 = s.row[a2];
                                 fold<MODE, EC1>(s, args, R.b0 + A1.thr + A2.thr, R.b1 + A1.acc + A2.acc,
                                            R.b2 + A1.en + A2.en, R.b3 + A1.idle + A2.idle,
-                                           dmax(s.lat_by_rank[R.top], dmax(s.lat_e[a1], s.lat_e[a2])),
+                                           dmax(s.lat_by_rank[R.top], dmax(s.lat_e[a1], s.lat_e[a2])), mcnt,
                                            R.ibase + (int)(ent >> 17), rS, rV, rP, args.seed,
                                            gchain, (uint64_t)k);
                             }
@@ -686,7 +691,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             S0 += x * s.row[e].thr; S1 += x * s.row[e].acc; S2 += x * s.row[e].en; S3 += x * s.row[e].idle;
             if (x > 0) m |= s.rbit[e];
         }
-        const Score sb = epilogue_d(S0, S1, S2, S3, lmax_of(s, m), s.ec);
+        const Score sb = epilogue_d(S0, S1, S2, S3, lmax_of(s, m), s.mcount, s.ec);   // moves keep m
         r.f = sb.f; r.h = sb.h; r.p95_ms = sb.L; r.accuracy = sb.A; r.energy_wh = sb.E;
         r.sla_met = sb.sla;
         r.status = status; r.steps = steps; r.best_step = best_step;

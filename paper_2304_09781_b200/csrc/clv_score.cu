@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(SNT) score_graphs_kernel(const __grid_constant
             const long long i = base + threadIdx.x;
             const bool feas = !memfail && m != 0 && feasible(a.F, n, sv[0], sv[1], sv[2], sv[3], sv[4]);
             if (feas) {
-                Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)], a.ec);
+                Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)],
+                                    (double)(sv[0] + sv[1] + sv[2] + sv[3] + sv[4]), a.ec);
                 ++c_valid;
                 c_sla += sc.sla;
                 consider(r0, r1, sc, a.index_base + i, a.select_mode);
@@ -265,7 +266,8 @@ __global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_cons
             const bool feas = !(pe[c] & R.bad) && pe[c] != 0 &&
                               feasible(a.F, n, sv[c][0], sv[c][1], sv[c][2], sv[c][3], sv[c][4]);
             if (feas) {
-                Score sc = epilogue_d(S0[c], S1[c], S2[c], S3, lmax, a.ec);
+                Score sc = epilogue_d(S0[c], S1[c], S2[c], S3, lmax,
+                                      (double)(sv[c][0] + sv[c][1] + sv[c][2] + sv[c][3] + sv[c][4]), a.ec);
                 ++c_valid;
                 c_sla += sc.sla;
                 consider(r0, r1, sc, a.index_base + i, a.select_mode);
@@ -405,7 +407,8 @@ __global__ void __launch_bounds__(SNT) score_x_kernel(const __grid_constant__ Sc
                 if (atomicCAS(a.error_flag, 0, err) == 0) *a.error_index = c;
                 if (a.sla_out) a.sla_out[c] = 0;
             } else {
-                Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)], a.ec);
+                Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)],
+                                    (double)(off1 - off0), a.ec);
                 ++c_valid;
                 c_sla += sc.sla;
                 consider(r0, r1, sc, a.index_base + c, a.select_mode);
@@ -455,7 +458,8 @@ __global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ Ora
             S0 += row[e].thr; S1 += row[e].acc; S2 += row[e].en; S3 += row[e].idle;
             m |= 1ULL << rank[e];
         }
-        Score sc = epilogue(S0 * n, S1 * n, S2 * n, S3 * n, lat_by_rank[63 - __clzll((long long)m)], a.ec);
+        Score sc = epilogue(S0 * n, S1 * n, S2 * n, S3 * n, lat_by_rank[63 - __clzll((long long)m)],
+                            (double)(n * ns), a.ec);
         ++c_valid;
         c_sla += sc.sla;
         consider(r0, r1, sc, i, CLV_SELECT_ORACLE);
@@ -547,7 +551,7 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
             // slice's variant draw.  The body is branch-free (a configuration draw adds the
             // all-zero row), so lanes stay converged until their last GPU.
             const int ng = a.pods[p].n_gpus;
-            int g = 0, rem = 0, r = 0, slot = 0;
+            int g = 0, rem = 0, r = 0, slot = 0, inst = 0;
             while (rem != 0 || g < ng) {
                 const uint32_t w = d.next();
                 const bool cfg = rem == 0;
@@ -562,8 +566,10 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
                 rem = cfg ? (int)nsl[rn] : rem - 1;
                 slot = cfg ? 0 : slot + 1;
                 g += cfg ? 1 : 0;
+                inst += cfg ? 0 : 1;
             }
-            Score sc = epilogue_d(S0, S1, S2, S3, lat_by_rank[p][63 - __clzll((long long)m)], a.pods[p].ec);
+            Score sc = epilogue_d(S0, S1, S2, S3, lat_by_rank[p][63 - __clzll((long long)m)], (double)inst,
+                                  a.pods[p].ec);
             const double wt = a.pods[p].weight;
             if (p == 0) { f = wt * sc.f; h = wt * sc.h; }
             else { f = f + wt * sc.f; h = h + wt * sc.h; }

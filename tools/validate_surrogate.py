@@ -39,6 +39,18 @@ def surrogate_AE(W, tables, sc):
     return A, E
 
 
+def many_server_L(W, tables, sc, mode):
+    """Candidate p95 models on the host: Lmax * (1 + rho^k / (m (1 - rho))) with k = 8 or sqrt(2(m+1))."""
+    W = W.astype(np.float64)
+    thr = W @ np.asarray(tables.thr_q, dtype=np.float64)
+    lat = np.asarray(tables.lat95, dtype=np.float64)
+    lmax = np.where(W > 0, lat[None, :], 0.0).max(axis=1)
+    rho = np.minimum(np.ldexp(sc.arrival_rps, tables.kt) / thr, sc.rho_sat)
+    m = W.sum(axis=1)
+    k = 8.0 if mode == "k8" else np.sqrt(2.0 * (m + 1.0))
+    return lmax * (1.0 + rho ** k / (m * (1.0 - rho)))
+
+
 def spearman(a, b):
     ra = np.argsort(np.argsort(a)).astype(np.float64)
     rb = np.argsort(np.argsort(b)).astype(np.float64)
@@ -56,7 +68,17 @@ def compare(name, fleets, eng, prof, sc, w, l_tail_des):
     dE = np.array([r.energy_wh_total / r.completed for r in reps])
     dP = np.array([r.p95_ms for r in reps])
     sla_d = dP <= l_tail_des
+    base_W = np.array([build_graph(base_config(64, prof), prof).weights], dtype=np.uint16)
+    alt = {}
+    for mode in ("k8", "sakasegawa"):
+        Lm = many_server_L(W, prof.scoring_tables(), sc, mode)
+        lt = many_server_L(base_W, prof.scoring_tables(), sc, mode)[0]
+        s_m = Lm <= lt
+        alt[mode] = {"p95_spearman": spearman(Lm, dP), "l_tail_ms": float(lt), "p95_median_ms": float(np.median(Lm)),
+                     "sla_agreement": float(np.mean(s_m == sla_d)), "sla_meet": int(s_m.sum()),
+                     "median_rel_err": float(np.median(np.abs(Lm - dP) / dP))}
     return {
+        "many_server_models": alt,
         "population": name, "fleets": len(fleets),
         "accuracy_mean_abs_diff": float(np.mean(np.abs(A - dA))),
         "accuracy_max_abs_diff": float(np.max(np.abs(A - dA))),
