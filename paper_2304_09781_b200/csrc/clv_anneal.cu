@@ -113,6 +113,9 @@ struct __align__(16) AnnealSmem {
     // per-step tables (the pair entries live in the dynamic tail)
     RemEnt se[CLV_MAX_EDGES];
     int nPE, nRP, nLen;
+    unsigned char pe_list[CLV_MAX_EDGES];  // present edges, ascending
+    int pfx[CLV_MAX_EDGES + 1];            // removal pairs starting before present edge i
+    int pk[MAXP];                          // available pair q: P | x << 10 | y << 16
     int warp_off[NWARP + 1], warp_len[NWARP + 1];
     int fsvec[CLV_K];                      // slice vector the feasibility bytes belong to
     unsigned char feasS[25];
@@ -218,7 +221,10 @@ __device__ __forceinline__ unsigned char top_rank(unsigned long long m) {
 // the move space by table position), the present-edge entries, and -- only when
 // the centre's slice multiset changed -- the feasibility bytes of all 25 single /
 // 625 double slice deltas (loads issued first so their latency overlaps the rest).
-__device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, int n, const FeasView &F) {
+template <bool PROF>
+__device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, int n, const FeasView &F,
+                                             long long *pacc) {
+    const long long pt0 = PROF ? clock64() : 0;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int NP = E * (E + 1) / 2;
     constexpr int PER = (MAXP + ANT - 1) / ANT;    // consecutive pairs per thread (4 at E <= 40)
@@ -263,43 +269,91 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
 #pragma unroll
         for (int q = 0; q < 3; ++q) fres[q] = cand[q] && ((word[q] >> bit[q]) & 1u);
     }
-    const int p0 = threadIdx.x * PER;
-    int cnt = 0, lsum = 0;
+    // (1) warp 0: present-edge list (ascending) and, per present edge i, the exclusive
+    //     prefix of the removal pairs that start at it: (e_i, e_i) when w >= 2, then
+    //     (e_i, e_j) for j > i -- i.e. the available pairs in ascending P(x, y), the
+    //     same deterministic order in every CTA of the cluster.
+    if (wid == 0) {
+        int k = 0;
+        for (int e0 = 0; e0 < E; e0 += 32) {
+            const int e = e0 + lane;
+            const bool ok = e < E && s.w[e] > 0;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
+            if (ok) s.pe_list[k + __popc(bal & ((1u << lane) - 1u))] = (unsigned char)e;
+            k += __popc(bal);
+        }
+        __syncwarp();
+        int pb = 0;
+        for (int i0 = 0; i0 < k; i0 += 32) {
+            const int i = i0 + lane;
+            const int c = i < k ? (k - i - 1) + (s.w[s.pe_list[i]] >= 2 ? 1 : 0) : 0;
+            int x = c;
 #pragma unroll
-    for (int p = p0; p < p0 + PER; ++p) {
-        if (p >= NP) break;
-        const int x = s.pair_tab[p] & 0xFF, y = s.pair_tab[p] >> 8;
-        const bool ok = (x == y) ? (s.w[x] >= 2) : (s.w[x] > 0 && s.w[y] > 0);
-        if (ok) { ++cnt; lsum += s.pair_len[p]; }
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+                if (lane >= d) x += y;
+            }
+            if (i < k) s.pfx[i] = pb + x - c;
+            pb += __shfl_sync(0xFFFFFFFFu, x, 31);
+        }
+        if (lane == 0) { s.nPE = k; s.pfx[k] = pb; s.nRP = pb; }
     }
-    int ic = cnt, il = lsum;                       // block exclusive scan in thread order
+    __syncthreads();
+    // (2) every thread: a contiguous run of <= PER available pairs, their move-list
+    //     lengths, and a block exclusive scan of the lengths in pair order.
+    const int k = s.nPE, npairs = s.nRP;
+    const int per = (npairs + ANT - 1) / ANT;
+    const int q0 = threadIdx.x * per;
+    int cnt = 0, lsum = 0;
+    if (q0 < npairs) {
+        int lo = 0, hi = k - 1;                    // last i with pfx[i] <= q0
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s.pfx[mid] <= q0) lo = mid; else hi = mid - 1;
+        }
+        int i = lo;
+#pragma unroll 1
+        for (int u = 0; u < PER; ++u) {
+            const int q = q0 + u;
+            if (u < per && q < npairs) {
+                while (q >= s.pfx[i + 1]) ++i;
+                const int x = s.pe_list[i];
+                const int y = s.pe_list[i + (q - s.pfx[i]) + (s.w[x] >= 2 ? 0 : 1)];
+                const int p = x * E - (x * (x - 1)) / 2 + (y - x);
+                s.pk[q] = p | (x << 10) | (y << 16);     // p < 1024; x, y < 64
+                lsum += s.pair_len[p];
+                ++cnt;
+            }
+        }
+    }
+    int il = lsum;                                 // block exclusive scan of lsum in thread order
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        const int yc = __shfl_up_sync(0xFFFFFFFFu, ic, d), yl = __shfl_up_sync(0xFFFFFFFFu, il, d);
-        if (lane >= d) { ic += yc; il += yl; }
+        const int yl = __shfl_up_sync(0xFFFFFFFFu, il, d);
+        if (lane >= d) il += yl;
     }
-    if (lane == 31) { s.warp_off[wid] = ic; s.warp_len[wid] = il; }
+    if (lane == 31) s.warp_len[wid] = il;
     __syncthreads();
     if (threadIdx.x < 32) {
-        const int c = lane < NWARP ? s.warp_off[lane] : 0, l = lane < NWARP ? s.warp_len[lane] : 0;
-        int c2 = c, l2 = l;
+        const int l = lane < NWARP ? s.warp_len[lane] : 0;
+        int l2 = l;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const int yc = __shfl_up_sync(0xFFFFFFFFu, c2, d), yl = __shfl_up_sync(0xFFFFFFFFu, l2, d);
-            if (lane >= d) { c2 += yc; l2 += yl; }
+            const int yl = __shfl_up_sync(0xFFFFFFFFu, l2, d);
+            if (lane >= d) l2 += yl;
         }
-        if (lane < NWARP) { s.warp_off[lane] = c2 - c; s.warp_len[lane] = l2 - l; }
-        if (lane == NWARP - 1) { s.nRP = c2; s.nLen = l2; }
+        if (lane < NWARP) s.warp_len[lane] = l2 - l;
+        if (lane == NWARP - 1) s.nLen = l2;
     }
     __syncthreads();
-    int pos = s.warp_off[wid] + ic - cnt, lpos = s.warp_len[wid] + il - lsum;
+    const long long pt1 = PROF ? clock64() : 0;
+    // (3) the removal entries (pairs: every thread; singles: the last warp)
+    int lpos = s.warp_len[wid] + il - lsum;
 #pragma unroll 1
-    for (int p = p0; p < p0 + PER; ++p) {
-        if (p >= NP) break;
-        const int x = s.pair_tab[p] & 0xFF, y = s.pair_tab[p] >> 8;
-        const bool ok = (x == y) ? (s.w[x] >= 2) : (s.w[x] > 0 && s.w[y] > 0);
-        if (!ok) continue;
-        RemEnt &r = rp[pos++];
+    for (int u = 0; u < cnt; ++u) {
+        const int pkv = s.pk[q0 + u];
+        const int p = pkv & 1023, x = (pkv >> 10) & 63, y = pkv >> 16;
+        RemEnt &r = rp[q0 + u];
         r.b0 = s.S[0] + -(s.row[x].thr + s.row[y].thr);
         r.b1 = s.S[1] + -(s.row[x].acc + s.row[y].acc);
         r.b2 = s.S[2] + -(s.row[x].en + s.row[y].en);
@@ -319,24 +373,17 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
         r.code = (unsigned short)(s.sl[x] * 125 + s.sl[y] * 25);
         r.r1 = (unsigned char)x; r.r2 = (unsigned char)y;
     }
-    if (wid == NWARP - 1) {                        // warp 0 runs the second-level scan above
-        int c = 0;
-        for (int e0 = 0; e0 < E; e0 += 32) {
-            const int e = e0 + lane;
-            const bool ok = e < E && s.w[e] > 0;
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
-            if (ok) {
-                RemEnt &r = s.se[c + __popc(bal & ((1u << lane) - 1u))];
-                r.b0 = s.S[0] + -s.row[e].thr; r.b1 = s.S[1] + -s.row[e].acc;
-                r.b2 = s.S[2] + -s.row[e].en; r.b3 = s.S[3] + -s.row[e].idle;
-                r.top = top_rank((s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask);
-                r.ibase = e * E;
-                r.code = (unsigned short)(s.sl[e] * 5);
-                r.r1 = (unsigned char)e; r.r2 = 0xFF; r.offm = 0; r.end = 0; r.pre = 0;
-            }
-            c += __popc(bal);
+    if (wid == NWARP - 1) {
+        for (int i = lane; i < k; i += 32) {
+            const int e = s.pe_list[i];
+            RemEnt &r = s.se[i];
+            r.b0 = s.S[0] + -s.row[e].thr; r.b1 = s.S[1] + -s.row[e].acc;
+            r.b2 = s.S[2] + -s.row[e].en; r.b3 = s.S[3] + -s.row[e].idle;
+            r.top = top_rank((s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask);
+            r.ibase = e * E;
+            r.code = (unsigned short)(s.sl[e] * 5);
+            r.r1 = (unsigned char)e; r.r2 = 0xFF; r.offm = 0; r.end = 0; r.pre = 0;
         }
-        if (lane == 0) s.nPE = c;
     }
     if (refresh) {
         for (int q = 0; q < 3; ++q) {
@@ -347,6 +394,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
         if (threadIdx.x < CLV_K) s.fsvec[threadIdx.x] = s.svec[threadIdx.x];
     }
     __syncthreads();
+    if (PROF && threadIdx.x == 0) { pacc[10] += pt1 - pt0; pacc[11] += clock64() - pt1; }
 }
 
 // Exact score of one neighbour folded into the thread's records.
@@ -387,7 +435,7 @@ __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : 
 
 template <int MODE, int MINB, int UNR, bool PROF = false, bool EC1 = false>
 __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
-    long long prof_acc[PROF_SLOTS] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long prof_acc[PROF_SLOTS] = {};
     long long prof_last = 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     AnnealSmem &s = *reinterpret_cast<AnnealSmem *>(smem_raw);
@@ -483,7 +531,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             for (int q = 0; q < CLV_K; ++q) refreshed |= (s.svec[q] != s.fsvec[q]);
         }
         const long long prep0 = PROF ? clock64() : 0;
-        prepare_step(s, rp, E, n, args.F);
+        prepare_step<PROF>(s, rp, E, n, args.F, prof_acc);
         if (PROF && threadIdx.x == 0 && refreshed) { prof_acc[7] += clock64() - prep0; prof_acc[8] += 1; }
         PROF_MARK(1);
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();

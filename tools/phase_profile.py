@@ -19,7 +19,7 @@ from paper_2304_09781_b200.engine import CloverEngine  # noqa: E402
 from paper_2304_09781_b200.objective import AnnealParams  # noqa: E402
 from paper_2304_09781_b200.profiles import synthetic_profile  # noqa: E402
 
-SLOTS = 10
+SLOTS = 12
 NAMES = ["prepare", "score", "cta_reduce", "sync1", "leader", "sync2", "apply"]
 
 eng = CloverEngine(n_max=64)
@@ -43,6 +43,8 @@ other = {k: int(per_step(buf[:, 1, q])) for q, k in enumerate(NAMES)}
 nref = buf[:, 0, 8].sum()
 print("cluster %d cycles/step leader CTA: %s\n  rank-1 CTA: %s" % (cl, lead, other))
 print("leader: apply_move %d cycles per step" % per_step(buf[:, 0, 9]))
+print("prepare: refresh + pair count + scans %d, entry build + singles %d cycles per step"
+      % (per_step(buf[:, 0, 10]), per_step(buf[:, 0, 11])))
 print("feasibility refresh in %.1f%% of steps; prepare cycles per refresh step %d, per other step %d"
       % (100.0 * nref / steps.sum(), buf[:, 0, 7].sum() / max(nref, 1),
          (buf[:, 0, 0].sum() - buf[:, 0, 7].sum()) / max(steps.sum() - nref, 1)))
