@@ -165,7 +165,13 @@ class CloverEngine:
         self._check(self.lib.clv_set_profile(self.ctx, fam, t.variant_count, thr.ctypes.data, acc.ctypes.data,
                                              en.ctypes.data, idle.ctypes.data, lat.ctypes.data, mem.ctypes.data,
                                              t.kt, t.ke, t.ki))
-        self._set_sim_profile(fam, profile)
+        try:
+            self._set_sim_profile(fam, profile)
+            sim_error = None
+        except CarbonSchedError as exc:     # e.g. > 6 lognormal sigmas: only the simulator refuses
+            sim_error = exc
+        self._sim_errors = getattr(self, "_sim_errors", {})
+        self._sim_errors[key] = sim_error
         self._families[key] = (fam, profile, t)
         lru.append(key)
         return fam
@@ -463,6 +469,9 @@ class CloverEngine:
         None, instance_counts [total] or None, n_requests)."""
         torch = self.torch
         fam = self.add_profile(profile)
+        err = getattr(self, "_sim_errors", {}).get(self._profile_key(profile))
+        if err is not None:
+            raise err
         dev = "cuda:%d" % self.device
         if not isinstance(inst_edges, torch.Tensor):
             inst_edges = torch.from_numpy(np.ascontiguousarray(inst_edges, dtype=np.uint8)).to(dev)

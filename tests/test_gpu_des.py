@@ -164,3 +164,43 @@ def test_run_trace_with_des_confirmation(engine, tmp_path):
                       des_window_s=120.0, des_top=8)
     R.write_timeline_csv(str(tmp_path / "t2.csv"), again)
     assert open(tmp_path / "t2.csv").read() == open(tmp_path / "timeline.csv").read()
+
+
+def test_parity_ties_and_many_sigma_classes(engine):
+    """Deterministic service on identical instances (every dispatch is a tie on free time,
+    broken by instance order) and a catalog whose lognormal rows use several sigmas
+    (one multiplier class each)."""
+    vs = [VariantSpec(v, 0.7 + 0.03 * v, 1.0) for v in range(1, 5)]
+    det = {(v, s): ServiceRow(12.0, "deterministic", 0.0, 0.002) for v in range(1, 5) for s in SliceType}
+    pd = ProfileTable("ties", vs, det, {s: 3.0 for s in SliceType})
+    fc = FleetConfig([19, 19], [1, 2, 3, 4, 1, 2, 3] * 2, pd.topology)
+    sim = des.sim_input(pd)
+    for periodic, rate in ((True, 400.0), (False, 300.0)):
+        w = S.Workload(rate, 5.0, 4, periodic=periodic, warmup=13)
+        r = S.simulate(fc, pd, w, engine=engine)
+        ref = des.simulate(des.fleet_edges(fc), sim, rate, 5.0, 4, periodic=periodic, warmup=13)
+        assert_same(r, ref, "ties periodic=%s" % periodic)
+    sig = {}
+    for v in range(1, 5):
+        for s in SliceType:
+            sig[(v, s)] = ServiceRow(8.0 + v, "lognormal", 0.1 * v + (0.05 * (s.index % 2) if v < 3 else 0.0), 0.001)
+    pl = ProfileTable("sigmas", vs, sig, {s: 2.0 for s in SliceType})
+    fleets = random_fleets(pl, 3, 5, 12)
+    w = S.Workload(250.0, 20.0, 9)
+    reps = S.simulate_fleets(fleets, pl, w, engine=engine)
+    siml = des.sim_input(pl)
+    for c, f in enumerate(fleets):
+        assert_same(reps[c], des.simulate(des.fleet_edges(f), siml, 250.0, 20.0, 9), "sigmas %d" % c)
+
+
+def test_too_many_sigma_classes_only_blocks_simulation(engine):
+    from paper_2304_09781_b200.errors import ProfileError
+    vs = [VariantSpec(v, 0.7 + 0.03 * v, 1.0) for v in range(1, 5)]
+    sig = {(v, s): ServiceRow(8.0 + v, "lognormal", 0.1 * v + 0.05 * (s.index % 2), 0.001)
+           for v in range(1, 5) for s in SliceType}                     # 8 distinct sigmas
+    p = ProfileTable("sigmas8", vs, sig, {s: 2.0 for s in SliceType})
+    fc = FleetConfig([1, 1], [1, 4], p.topology)
+    best, _ = engine.score_fleets([fc], p, engine.calibrate(p, 2, 300.0, 0.5))
+    assert best["found"]
+    with pytest.raises(ProfileError):
+        S.simulate(fc, p, S.Workload(50.0, 10.0, 1), engine=engine)
