@@ -796,7 +796,8 @@ cudaError_t launch_anneal(const AnnealArgs &a, int cluster_size, cudaStream_t st
         switch (env_int("CLV_ANNEAL_VARIANT", 0)) {
             case 1: return launch_mode<MODE_BEST_ALL, 3, 1>(a, cluster_size, st);
             case 2: return launch_mode<MODE_BEST_ALL, 4, 1>(a, cluster_size, st);
-            case 3: return launch_mode<MODE_BEST_ALL, 2, 2>(a, cluster_size, st);
+            case 3: return launch_mode<MODE_BEST_ALL, 3, 3>(a, cluster_size, st);
+            case 4: return launch_mode<MODE_BEST_ALL, 3, 4>(a, cluster_size, st);
             case 9: return launch_mode<MODE_BEST_ALL, 3, 2, true>(a, cluster_size, st);
             default: return launch_mode<MODE_BEST_ALL, 3, 2>(a, cluster_size, st);
         }
