@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 #include "clv_ctx.h"
 
@@ -312,7 +313,67 @@ __host__ __device__ inline size_t slab_bytes(int kmax) {
     return ((size_t)SIM_MAX_CLS * 32 * 8 + (size_t)kmax * 22 + 15) & ~(size_t)15;
 }
 
-template <bool RAND>
+// Queue recursion with the instance keys in registers (K <= 32 * S): lane l owns
+// instances l + 32 t (t < S) and their minimum; each request is a 2-step redux.sync
+// argmin over the lane minima, a warp-uniform service lookup, and -- in the owner lane
+// only -- a register update plus an S-wide min tree (no shared-memory round trip and no
+// second reduction on the dependency chain).
+template <bool RAND, int S>
+__device__ __forceinline__ void run_sim_regs(const Slab &q, const SimArgs &args, int K, long long N, int C,
+                                             long long *cs, unsigned short *js, int lane) {
+    unsigned long long k[S];
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+        const int j = lane + 32 * t;
+        k[t] = j < K ? (unsigned long long)j : ~0ULL;
+    }
+    unsigned long long lm = k[0];                  // keys start at j: slot 0 is the lane's minimum
+    for (long long b = 0; b < N; b += 32) {
+        const long long i = b + lane;
+        const long long al = i < N ? __ldg(args.a + i) : 0LL;
+        if (RAND) {
+            __syncwarp();
+            for (int c2 = 0; c2 < C; ++c2)
+                q.mst[c2 * 32 + lane] = i < N ? __ldg(args.mult + (size_t)c2 * N + i) : 1.0;
+            __syncwarp();
+        }
+        const int nb = (int)min(32LL, N - b);
+        long long myc = 0;
+        unsigned myj = 0;
+#pragma unroll 4
+        for (int r = 0; r < nb; ++r) {
+            const long long ai = __shfl_sync(0xFFFFFFFFu, al, r);
+            const unsigned hi = (unsigned)(lm >> 32);
+            const unsigned mh = __reduce_min_sync(0xFFFFFFFFu, hi);
+            const unsigned ml = __reduce_min_sync(0xFFFFFFFFu, hi == mh ? (unsigned)lm : 0xFFFFFFFFu);
+            const int j = (int)(ml & 2047u);
+            const long long fv = (long long)((((unsigned long long)mh << 32) | ml) >> 11);
+            long long sv;
+            if (RAND) sv = round_ns(__longlong_as_double(q.svc[j]) * q.mst[q.cls[j] * 32 + r]);
+            else sv = q.svc[j];
+            const long long c = (ai > fv ? ai : fv) + sv;
+            if (lane == (j & 31)) {
+                const unsigned long long np = ((unsigned long long)c << 11) | (unsigned)j;
+                const int ts = j >> 5;
+                unsigned long long tm[S];
+#pragma unroll
+                for (int t = 0; t < S; ++t) {
+                    if (t == ts) k[t] = np;
+                    tm[t] = k[t];
+                }
+#pragma unroll
+                for (int w = S / 2; w >= 1; w /= 2)
+#pragma unroll
+                    for (int t = 0; t < w; ++t) tm[t] = tm[t] < tm[t + w] ? tm[t] : tm[t + w];
+                lm = tm[0];
+            }
+            if (lane == r) { myc = c; myj = (unsigned)j; }
+        }
+        if (i < N) { cs[i] = myc; js[i] = (unsigned short)myj; }
+    }
+}
+
+template <bool RAND, int S>
 __global__ void __launch_bounds__(SNT) sim_kernel(const __grid_constant__ SimArgs args) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SimFamily F;
@@ -363,7 +424,9 @@ __global__ void __launch_bounds__(SNT) sim_kernel(const __grid_constant__ SimArg
                 else if (bad & 1) status = CLV_ERR_INFEASIBLE_ASSIGNMENT;
             }
             __syncwarp();
-            if (status == 0) {
+            if (status == 0 && S > 0) {
+                run_sim_regs<RAND, (S > 0 ? S : 1)>(q, args, K, N, C, cs, js, lane);
+            } else if (status == 0) {
                 // Slot j holds the packed key (free_j << 11) | j (unique, order-preserving: the
                 // argmin key is argmin (free, j)); lane g caches the minimum of instance group
                 // g = {g, g+32, ...}; slot j is read and written only by lane j >> 5.
@@ -690,7 +753,26 @@ int clv_simulate(clv_ctx *ctx, int family, const clv_workload *w, int64_t count,
         sim_mult_kernel<<<std::max(g, 1), 256, 0, st>>>(S->fam_dev + family, S->ex, S->z, N, S->mult);
         SIM_CUDA(cudaGetLastError(), "sim multipliers");
     }
-    auto kern = rnd ? sim_kernel<true> : sim_kernel<false>;
+    // register-resident keys when every fleet has <= 512 instances (S slots per lane)
+    // register-resident keys for small fleets; CLV_SIM_SLOTS caps the slots per lane
+    // (0 = always the shared-memory group layout)
+    int cap = 2;                                   // measured: registers win up to 2 slots (tools/des_slots.py)
+    if (const char *ev = getenv("CLV_SIM_SLOTS")) cap = atoi(ev);
+    int slots = max_instances <= 32 ? 1 : max_instances <= 64 ? 2 : max_instances <= 128 ? 4
+              : max_instances <= 256 ? 8 : max_instances <= 512 ? 16 : 0;
+    if (slots > cap) slots = 0;
+    auto pick = [&](auto r) {
+        constexpr bool R = decltype(r)::value;
+        switch (slots) {
+            case 1: return sim_kernel<R, 1>;
+            case 2: return sim_kernel<R, 2>;
+            case 4: return sim_kernel<R, 4>;
+            case 8: return sim_kernel<R, 8>;
+            case 16: return sim_kernel<R, 16>;
+            default: return sim_kernel<R, 0>;
+        }
+    };
+    auto kern = rnd ? pick(std::true_type{}) : pick(std::false_type{});
     SIM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn), "sim smem");
     int occ = 0;
     SIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SNT, dyn), "sim occupancy");
