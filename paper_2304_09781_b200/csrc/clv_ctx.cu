@@ -432,7 +432,7 @@ int clv_score_x(clv_ctx *ctx, int family, int n, const uint8_t *xp_dev, const ui
     a.xp = xp_dev; a.xv = xv_dev; a.xv_off = xv_off_dev; a.topo = ctx->topo_dev;
     a.f_out = f_dev; a.h_out = h_dev; a.sla_out = sla_dev; a.sel = make_sel(ctx);
     a.error_flag = ctx->err_flag; a.error_index = ctx->err_index;
-    CLV_CUDA(launch_score_x(a, n, grid_for(ctx, count, 8), st), "score_x");
+    CLV_CUDA(launch_score_x(a, n, grid_for(ctx, count, 256), st), "score_x");
     CLV_CUDA(cudaMemcpyAsync(ctx->host_err, ctx->err_flag, sizeof(int), cudaMemcpyDeviceToHost, st), "copy err");
     CLV_CUDA(cudaMemcpyAsync(ctx->host_err + 2, ctx->err_index, sizeof(long long), cudaMemcpyDeviceToHost, st), "copy err idx");
     rc = fetch_best(ctx, select_mode, st, best);

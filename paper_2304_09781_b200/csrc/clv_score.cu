@@ -330,8 +330,11 @@ cudaError_t launch_score_graphs(const ScoreArgs &a, const FamilyTables &T, int g
 }
 
 // ----------------------------------------------------------------- score_x
-// One warp per candidate; lanes stride the GPUs, a shuffle scan of slice
-// counts gives each GPU's first assignment slot (FleetConfig layout, mig.py:240-242).
+// One THREAD per candidate: it walks its FleetConfig row (config id per GPU, then that
+// config's slices largest first, mig.py:240-242) and its variant bytes in order, adding
+// the exact integer rows.  Rows are read byte by byte through L1 (a candidate's bytes
+// are contiguous, so after the first touch of a 32-B sector the rest hit); slots are
+// processed four at a time so four variant loads are in flight per thread.
 __global__ void __launch_bounds__(SNT) score_x_kernel(const __grid_constant__ ScoreArgs a, int n) {
     __shared__ ERow row[CLV_MAX_EDGES];
     __shared__ double lat_by_rank[CLV_MAX_EDGES];
@@ -352,70 +355,48 @@ __global__ void __launch_bounds__(SNT) score_x_kernel(const __grid_constant__ Sc
     __syncthreads();
     const int V = T.V;
     const unsigned long long mem_ok = T.mem_ok;
-    const int lane = threadIdx.x & 31;
-    const long long warp0 = ((long long)blockIdx.x * SNT + threadIdx.x) >> 5;
-    const long long nwarps = ((long long)gridDim.x * SNT) >> 5;
     RecP r0 = recp_none(), r1 = recp_none();
     unsigned long long c_valid = 0, c_sla = 0;
-    for (long long c = warp0; c < a.count; c += nwarps) {
+    for (long long c = (long long)blockIdx.x * SNT + threadIdx.x; c < a.count; c += (long long)gridDim.x * SNT) {
         const uint8_t *xp = a.xp + c * n;
-        const long long off0 = a.xv_off[c], off1 = a.xv_off[c + 1];
+        const long long off0 = __ldg(a.xv_off + c), off1 = __ldg(a.xv_off + c + 1);
+        const uint8_t *xv = a.xv + off0;
+        const long long mcnt = off1 - off0;
         long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
         unsigned long long m = 0;
         int err = 0;
-        long long carry = 0;   // slots used by earlier 32-GPU chunks
-        for (int g0 = 0; g0 < n; g0 += 32) {
-            const int g = g0 + lane;
-            int r = -1, ns = 0;
-            if (g < n) {
-                r = row_of_id[xp[g]];
-                if (r < 0) err = CLV_ERR_INVALID_CONFIG; else ns = nsl[r];
-            }
-            int incl = ns;
+        long long slot = 0;
+        for (int g = 0; g < n && !err; ++g) {
+            const int r = row_of_id[__ldg(xp + g)];
+            if (r < 0) { err = CLV_ERR_INVALID_CONFIG; break; }
+            const int ns = nsl[r];
+            if (slot + ns > mcnt) { err = CLV_ERR_CARBON_SCHED; break; }
+            int vv[7];
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                int y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-                if (lane >= d) incl += y;
-            }
-            const long long pos = off0 + carry + (incl - ns);
-            for (int j = 0; j < ns; ++j) {
-                const long long q = pos + j;
-                if (q >= off1) { err = CLV_ERR_CARBON_SCHED; break; }
-                const int v = a.xv[q];
-                const int k = kinds[r][j];
-                if (v < 1 || v > V) { err = CLV_ERR_INFEASIBLE_ASSIGNMENT; break; }
-                const int e = (v - 1) * 5 + k;
-                if (!((mem_ok >> e) & 1ULL)) { err = CLV_ERR_INFEASIBLE_ASSIGNMENT; break; }
+            for (int j = 0; j < 7; ++j) vv[j] = j < ns ? (int)__ldg(xv + slot + j) : 1;
+#pragma unroll
+            for (int j = 0; j < 7; ++j) {
+                if (j >= ns) break;
+                const int v = vv[j];
+                const int e = (v - 1) * 5 + kinds[r][j];
+                if (v < 1 || v > V || !((mem_ok >> e) & 1ULL)) { err = CLV_ERR_INFEASIBLE_ASSIGNMENT; break; }
                 S0 += row[e].thr; S1 += row[e].acc; S2 += row[e].en; S3 += row[e].idle;
                 m |= 1ULL << rank[e];
             }
-            carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+            slot += ns;
         }
-#pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) {
-            S0 += __shfl_xor_sync(0xFFFFFFFFu, S0, d);
-            S1 += __shfl_xor_sync(0xFFFFFFFFu, S1, d);
-            S2 += __shfl_xor_sync(0xFFFFFFFFu, S2, d);
-            S3 += __shfl_xor_sync(0xFFFFFFFFu, S3, d);
-            m |= __shfl_xor_sync(0xFFFFFFFFu, m, d);
-            int e2 = __shfl_xor_sync(0xFFFFFFFFu, err, d);
-            err = err ? err : e2;
-        }
-        if (lane == 0) {
-            if (!err && carry != off1 - off0) err = CLV_ERR_CARBON_SCHED;   // length mismatch
-            if (err) {
-                if (atomicCAS(a.error_flag, 0, err) == 0) *a.error_index = c;
-                if (a.sla_out) a.sla_out[c] = 0;
-            } else {
-                Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)],
-                                    (double)(off1 - off0), a.ec);
-                ++c_valid;
-                c_sla += sc.sla;
-                consider(r0, r1, sc, a.index_base + c, a.select_mode);
-                if (a.f_out) a.f_out[c] = sc.f;
-                if (a.h_out) a.h_out[c] = sc.h;
-                if (a.sla_out) a.sla_out[c] = sc.sla;
-            }
+        if (!err && slot != mcnt) err = CLV_ERR_CARBON_SCHED;              // length mismatch
+        if (err) {
+            if (atomicCAS(a.error_flag, 0, err) == 0) *a.error_index = c;
+            if (a.sla_out) a.sla_out[c] = 0;
+        } else {
+            Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)], (double)mcnt, a.ec);
+            ++c_valid;
+            c_sla += sc.sla;
+            consider(r0, r1, sc, a.index_base + c, a.select_mode);
+            if (a.f_out) a.f_out[c] = sc.f;
+            if (a.h_out) a.h_out[c] = sc.h;
+            if (a.sla_out) a.sla_out[c] = sc.sla;
         }
     }
     grid_finish<SNT>(r0, r1, c_valid, c_sla, a.sel);

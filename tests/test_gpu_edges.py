@@ -117,3 +117,30 @@ def test_simulate_empty_batch(engine):
                                          S.Workload(100.0, 10.0, 1))
     assert len(reps) == 0 and nreq > 0
     assert S.simulate_fleets([], prof, S.Workload(100.0, 10.0, 1), engine=engine) == []
+
+
+def test_score_x_error_paths(engine):
+    from paper_2304_09781_b200.errors import CarbonSchedError, InfeasibleAssignmentError, InvalidConfigError
+    from paper_2304_09781_b200.mig import FleetConfig
+    prof = synthetic_profile("bert")                         # variant 6 (11 GB) does not fit 1g / 2g
+    T = OracleTables.from_profile(prof)
+    sc = calibrate(prof, T, 2, 300.0, 0.5)
+    good = [FleetConfig([1, 19], [3] + [1] * 7), FleetConfig([5, 9], [2] * (len(DEFAULT_TOPOLOGY.config_slices(5))
+                                                                        + len(DEFAULT_TOPOLOGY.config_slices(9))))]
+
+    def csr(fleets, patch=None):
+        xp = np.array([f.partitions for f in fleets], dtype=np.uint8)
+        xvs = [np.array(f.assignments, dtype=np.uint8) for f in fleets]
+        if patch:
+            patch(xp, xvs)
+        off = np.concatenate([[0], np.cumsum([len(x) for x in xvs])]).astype(np.int64)
+        return xp, np.concatenate(xvs), off
+
+    best, _ = engine.score_x(*csr(good), 2, prof, sc)
+    assert best["valid_count"] == 2
+    with pytest.raises(InvalidConfigError):
+        engine.score_x(*csr(good, lambda xp, xv: xp.__setitem__((1, 0), 200)), 2, prof, sc)
+    with pytest.raises(CarbonSchedError):
+        engine.score_x(*csr(good, lambda xp, xv: xv.__setitem__(0, xv[0][:-1])), 2, prof, sc)
+    with pytest.raises(InfeasibleAssignmentError):
+        engine.score_x(*csr(good, lambda xp, xv: xv[0].__setitem__(1, 6)), 2, prof, sc)

@@ -51,6 +51,23 @@ def main():
                 "GB_per_s": bytes_ / ms / 1e6, "hbm_peak_GBps": PEAKS["hbm_gbs"],
                 "frac": bytes_ / ms / 1e6 / PEAKS["hbm_gbs"], "bytes_per_candidate": W.shape[1] * 2})
     del W
+    # --- score_x from HBM: 1M FleetConfig CSR rows of an n=64 fleet (xp n B + xv m B + 8 B offset)
+    fl = random_fleets(eng, prof, n, 9, 4096, 0)
+    reps = 256
+    xp1 = np.array([f.partitions for f in fl], dtype=np.uint8)
+    xv1 = [np.array(f.assignments, dtype=np.uint8) for f in fl]
+    xp = np.tile(xp1, (reps, 1))
+    xvs = xv1 * reps
+    xv = np.concatenate(xvs)
+    off = np.zeros(len(xvs) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(x) for x in xvs])
+    xp_d, xv_d, off_d = torch.from_numpy(xp).cuda(), torch.from_numpy(xv).cuda(), torch.from_numpy(off).cuda()
+    cnt = len(xvs)
+    ms = timeit(lambda: eng.score_x(xp_d, xv_d, off_d, n, prof, sc, outputs=False), reps=5)
+    bytes_ = xp.nbytes + xv.nbytes + off.nbytes
+    out.append({"kernel": "score_x", "candidates": cnt, "ms": ms, "candidates_per_s": cnt / ms * 1e3,
+                "GB_per_s": bytes_ / ms / 1e6, "hbm_peak_GBps": PEAKS["hbm_gbs"],
+                "frac": bytes_ / ms / 1e6 / PEAKS["hbm_gbs"], "bytes_per_candidate": bytes_ / cnt})
     # --- oracle c0
     sc1 = eng.calibrate(prof, 1, 400.0, 0.5)
     tot = eng.oracle_size(prof)
