@@ -75,6 +75,8 @@ typedef struct clv_eval_params {
     double rho_sat;          /* queueing-factor saturation (0.999)               */
     int32_t strict_eq6;      /* 1 = verbatim Eq. 6 (CARBON_SCHED_STRICT_EQ6)     */
     int32_t n_gpus;          /* fleet size n                                     */
+    double max_accuracy_loss_pct; /* accuracy_threshold_mode: candidates with
+                                     dA < -max_loss count as SLA-violating; +inf = off */
 } clv_eval_params;
 
 /* Selected candidate of a scoring / search call. */

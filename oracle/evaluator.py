@@ -75,9 +75,11 @@ def epilogue(s_thr, s_acc, s_en, s_idle, lmax, m, tables, scenario) -> Evaluated
         dA = (A - a_base) * kA
         dC = 100.0 - E * kC
         f = lam * dC + (1.0 - lam) * dA
-        sla = L <= slo
+        lat_ok = L <= slo
+        # accuracy_threshold_mode: SLA class also needs dA >= -max_loss; h unchanged
+        sla = lat_ok & (dA >= -float(getattr(scenario, "max_accuracy_loss_pct", math.inf)))
         soft = np.where((f >= 0) | bool(scenario.strict_eq6), -f * (slo / L), -f * (L / slo))
-        h = np.where(sla, -f, soft)
+        h = np.where(lat_ok, -f, soft)
     return Evaluated(A, E, L, f, h, sla)
 
 

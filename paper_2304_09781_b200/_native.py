@@ -19,7 +19,7 @@ c_i32, c_i64, c_u64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint
 class EvalParams(ctypes.Structure):
     _fields_ = [("arrival_rps", c_f64), ("ci", c_f64), ("carbon_weight", c_f64),
                 ("base_accuracy", c_f64), ("base_carbon_g", c_f64), ("latency_slo_ms", c_f64),
-                ("rho_sat", c_f64), ("strict_eq6", c_i32), ("n_gpus", c_i32)]
+                ("rho_sat", c_f64), ("strict_eq6", c_i32), ("n_gpus", c_i32), ("max_accuracy_loss_pct", c_f64)]
 
 
 class Best(ctypes.Structure):

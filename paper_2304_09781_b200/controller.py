@@ -100,7 +100,8 @@ def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, pro
               lam: float = 0.5, ap: Optional[AnnealParams] = None, cp: ControllerParams = ControllerParams(),
               seed: int = 0, chains: int = 128, utilization: float = 0.7, strict_sla: bool = True,
               pue: float = 1.5, chain_base: int = 0, group=None, des_window_s: float = 0.0,
-              des_top: int = 16, log_evals: bool = False) -> TimelineReport:
+              des_top: int = 16, log_evals: bool = False,
+              max_acc_loss_pct: Optional[float] = None) -> TimelineReport:
     """Trace-driven control loop for ``scheme`` in SCHEMES.
 
     ``des_window_s`` > 0 turns on DES confirmation: L_tail_DES is the
@@ -109,7 +110,9 @@ def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, pro
     realized and simulated in one batch, and the first whose simulated p95 meets
     L_tail_DES is the candidate; every timeline row carries the simulated p95 of the
     active fleet.  ``log_evals`` keeps the winning chain's per-step log of the last
-    Clover re-plan (evals.csv)."""
+    Clover re-plan (evals.csv).  ``max_acc_loss_pct`` is accuracy_threshold_mode
+    (SPEC:612-627): candidates losing more accuracy than that count as SLA-violating
+    in best tracking, so the controller never deploys them."""
     import torch
     from .search import anneal_chains, base_config, co2opt_config
     if scheme not in SCHEMES:
@@ -118,6 +121,8 @@ def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, pro
     ci_mean = trace.mean()
     # L_tail and C_base from BASE at the trace's mean intensity (D7)
     base_sc = engine.calibrate(profile, n, ci_mean, lam, utilization, ci_base=ci_mean, pue=pue)
+    if max_acc_loss_pct is not None:
+        base_sc = replace(base_sc, max_accuracy_loss_pct=float(max_acc_loss_pct))
     base_w = np.array(build_graph(base_config(n, profile), profile).weights, dtype=np.int64)
     if scheme == "co2opt":
         w = np.array(build_graph(co2opt_config(n, profile), profile).weights, dtype=np.int64)

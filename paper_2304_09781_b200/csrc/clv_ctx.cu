@@ -59,6 +59,8 @@ int make_ec(clv_ctx *ctx, const clv_eval_params *p, const FamilyTables &T, EvalC
     ec.kA = 100.0 / p->base_accuracy;
     ec.kC = p->ci / (10.0 * p->base_carbon_g);
     ec.strict = p->strict_eq6 ? 1 : 0;
+    if (!(p->max_accuracy_loss_pct >= 0)) return fail(ctx, CLV_ERR_CARBON_SCHED, "max_accuracy_loss_pct must be >= 0");
+    ec.min_dA = -p->max_accuracy_loss_pct;
     ec.n = p->n_gpus;
     return CLV_OK;
 }

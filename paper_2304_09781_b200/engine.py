@@ -42,7 +42,7 @@ def eval_params(s: Scenario) -> N.EvalParams:
     o = s.obj
     return N.EvalParams(float(s.arrival_rps), float(s.ci), float(o.carbon_weight), float(o.base_accuracy),
                         float(o.base_carbon_g), float(o.latency_slo_ms), float(s.rho_sat),
-                        1 if s.strict_eq6 else 0, int(s.n_gpus))
+                        1 if s.strict_eq6 else 0, int(s.n_gpus), float(s.max_accuracy_loss_pct))
 
 
 @dataclass

@@ -123,6 +123,7 @@ class Scenario:
     obj: ObjectiveParams
     strict_eq6: bool = False
     rho_sat: float = RHO_SAT
+    max_accuracy_loss_pct: float = math.inf   # accuracy_threshold_mode; inf = off
 
     def with_lambda(self, lam: float) -> "Scenario":
         return replace(self, obj=replace(self.obj, carbon_weight=lam))
@@ -139,6 +140,8 @@ class Scenario:
             raise CarbonSchedError("carbon intensity must be finite and >= 0")
         if not 0.0 < self.rho_sat < 1.0:
             raise CarbonSchedError("rho_sat must be in (0,1)")
+        if not self.max_accuracy_loss_pct >= 0:
+            raise CarbonSchedError("max_accuracy_loss_pct must be >= 0 (inf = off)")
 
 
 PROPOSALS = ("best", "uniform")

@@ -21,7 +21,7 @@ class EvalParams(ctypes.Structure):
     _fields_ = [("arrival_rps", ctypes.c_double), ("ci", ctypes.c_double), ("carbon_weight", ctypes.c_double),
                 ("base_accuracy", ctypes.c_double), ("base_carbon_g", ctypes.c_double),
                 ("latency_slo_ms", ctypes.c_double), ("rho_sat", ctypes.c_double), ("strict_eq6", ctypes.c_int32),
-                ("n_gpus", ctypes.c_int32)]
+                ("n_gpus", ctypes.c_int32), ("max_accuracy_loss_pct", ctypes.c_double)]
 
 
 class Best(ctypes.Structure):
@@ -61,7 +61,7 @@ def test_reference_style_ctypes_binding_runs_the_oracle(engine):
         sc = engine.calibrate(prof, 1, 400.0, 0.5)
         o = sc.obj
         p = EvalParams(sc.arrival_rps, sc.ci, o.carbon_weight, o.base_accuracy, o.base_carbon_g, o.latency_slo_ms,
-                       sc.rho_sat, 1 if sc.strict_eq6 else 0, 1)
+                       sc.rho_sat, 1 if sc.strict_eq6 else 0, 1, float("inf"))
         best, total = Best(), ctypes.c_int64()
         rc = lib.clv_oracle_search(ctx, 0, 1, 0, -1, ctypes.byref(p), ctypes.byref(best), ctypes.byref(total), None)
         assert rc == 0, lib.clv_last_error(ctx)
