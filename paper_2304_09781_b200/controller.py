@@ -233,6 +233,9 @@ def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, pro
         replan_device_ms_max=float(np.max(tts)) if tts else 0.0,
         replan_wall_ms_mean=float(np.mean([r.wall_ms for r in rep.replans])) if tts else 0.0,
         candidates_scored=int(sum(r.evals for r in rep.replans)),
+        # share of the trace span spent optimising (here: measured re-plan wall time)
+        optimization_time_fraction_pct=100.0 * sum(r.wall_ms for r in rep.replans) / 1000.0
+        / max(steps * cp.trace_step_s, 1e-9),
         reconfigured_gpus=int(sum(r.changed_gpus for r in rep.replans)),
         downtime_gpu_s=float(sum(r.changed_gpus for r in rep.replans) * cp.reconfig_downtime_s))
     if des_window_s > 0:
