@@ -185,7 +185,7 @@ class AnnealParams:
     def step_limit(self) -> int:
         """Steps allowed: max_steps, and in 'proposal' mode the SPEC budget
         (stop once evaluations * eval_cost_s >= time_budget_s; the start counts)."""
-        if self.evaluate == "proposal" and self.eval_cost_s > 0:
+        if self.evaluate == "proposal" and self.eval_cost_s > 0 and math.isfinite(self.time_budget_s):
             evals = max(1, math.ceil(self.time_budget_s / self.eval_cost_s))
             return min(self.max_steps, evals - 1)
         return self.max_steps
