@@ -214,7 +214,7 @@ def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, pro
         reqs = sc.arrival_rps * cp.trace_step_s
         g_req = act["energy_wh"] / 1000.0 * ci * pue
         cum += reqs * g_req
-        cum_base += reqs * base["energy_wh"] / 1000.0 * ci * pue
+        cum_base += reqs * (base["energy_wh"] / 1000.0 * ci * pue)   # same op order as the active fleet
         acc_sum += act["accuracy"]
         row = dict(t=t, ci=ci, scheme=scheme, p95_ms=act["p95_ms"], sla_met=bool(act["sla_met"]),
                    accuracy=act["accuracy"], gco2_per_request=g_req, cumulative_gco2=cum, optimizing=optimizing)
