@@ -11,7 +11,9 @@ import os
 
 from . import errors as E
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libclover_b200.so")
+# CLV_LIB_PATH: an alternative in-tree build of the same ABI (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("CLV_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                           "libclover_b200.so")
 
 c_i32, c_i64, c_u64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
 
