@@ -109,6 +109,30 @@ def fleet_graph(partitions, assignments, topology, tables):
     return w
 
 
+def fleet_row_error(partitions, assignments, topology, tables):
+    """First error of one FleetConfig row, in the reference's order, or None.
+
+    FleetConfig.__init__ (reference mig.py:248-263): ``expected`` is summed over every
+    partition id (``config_slices`` raises InvalidConfigError for an unknown id, mig.py:
+    129-135), then the length is compared (CarbonSchedError), then ``any(v < 1)``
+    (CarbonSchedError).  Evaluation then rejects a variant above V or a
+    variant that does not fit its slice (InfeasibleAssignmentError).
+    Returns "invalid_config" | "length" | "variant_lt1" | "infeasible" | None.
+    """
+    known = set(int(c) for c in topology.config_ids)
+    if any(int(c) not in known for c in partitions):
+        return "invalid_config"
+    kinds = [k for cid in partitions for k in row_kinds(topology, int(cid))]
+    if len(kinds) != len(assignments):
+        return "length"
+    if any(int(v) < 1 for v in assignments):
+        return "variant_lt1"
+    for k, v in zip(kinds, assignments):
+        if int(v) > tables.V or not tables.mem_ok[(int(v) - 1) * 5 + k]:
+            return "infeasible"
+    return None
+
+
 # -- counter-RNG sweep -----------------------------------------------------------
 
 @dataclass

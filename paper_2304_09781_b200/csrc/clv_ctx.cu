@@ -429,21 +429,26 @@ int clv_score_x(clv_ctx *ctx, int family, int n, const uint8_t *xp_dev, const ui
     if (n < 1) return fail(ctx, CLV_ERR_CARBON_SCHED, "a fleet needs at least one GPU");
     cudaStream_t st = (cudaStream_t)stream;
     CLV_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
-    CLV_CUDA(cudaMemsetAsync(ctx->err_flag, 0, sizeof(int), st), "zero err");
+    CLV_CUDA(cudaMemsetAsync(ctx->err_index, 0xFF, sizeof(long long), st), "reset err key");
     a.fam = ctx->fam_dev + family; a.select_mode = select_mode; a.count = count; a.index_base = index_base;
     a.xp = xp_dev; a.xv = xv_dev; a.xv_off = xv_off_dev; a.topo = ctx->topo_dev;
     a.f_out = f_dev; a.h_out = h_dev; a.sla_out = sla_dev; a.sel = make_sel(ctx);
-    a.error_flag = ctx->err_flag; a.error_index = ctx->err_index;
+    a.error_key = reinterpret_cast<unsigned long long *>(ctx->err_index);
     CLV_CUDA(launch_score_x(a, n, grid_for(ctx, count, 256), st), "score_x");
-    CLV_CUDA(cudaMemcpyAsync(ctx->host_err, ctx->err_flag, sizeof(int), cudaMemcpyDeviceToHost, st), "copy err");
-    CLV_CUDA(cudaMemcpyAsync(ctx->host_err + 2, ctx->err_index, sizeof(long long), cudaMemcpyDeviceToHost, st), "copy err idx");
+    CLV_CUDA(cudaMemcpyAsync(ctx->host_err + 2, ctx->err_index, sizeof(long long), cudaMemcpyDeviceToHost, st), "copy err key");
     rc = fetch_best(ctx, select_mode, st, best);
     if (rc) return rc;
-    if (ctx->host_err[0]) {
-        long long idx;
-        std::memcpy(&idx, ctx->host_err + 2, sizeof(long long));
-        return fail(ctx, ctx->host_err[0], "candidate " + std::to_string(idx + index_base) +
-                                               ": invalid config id, variant or assignment length");
+    unsigned long long key;
+    std::memcpy(&key, ctx->host_err + 2, sizeof(key));
+    if (key != ~0ULL) {                       // lowest failing row, its first error (mig.py:248-263)
+        const long long idx = (long long)(key >> 8) + index_base;
+        const int code = (int)(key & 0xFF);
+        const std::string what = code == CLV_ERR_INVALID_CONFIG ? "unknown MIG partition id"
+                               : code == SCORE_X_VARIANT_LT1 ? "variant ordinals start at 1"
+                               : code == CLV_ERR_INFEASIBLE_ASSIGNMENT ? "variant out of range or does not fit its slice"
+                               : "assignment length does not match the slices implied by the partitions";
+        return fail(ctx, code == SCORE_X_VARIANT_LT1 ? CLV_ERR_CARBON_SCHED : code,
+                    "candidate " + std::to_string(idx) + ": " + what);
     }
     return CLV_OK;
 }

@@ -145,6 +145,10 @@ struct AnnealArgs {
     long long *prof;                // optional phase profile (debug variant only)
 };
 
+// score_x row error codes (low byte of ScoreArgs::error_key): the clv_status values, plus
+// CarbonSchedError's "variant ordinals start at 1" (mig.py:262) kept apart for its message.
+constexpr int SCORE_X_VARIANT_LT1 = 0x11;
+
 struct ScoreArgs {
     const FamilyTables *fam;
     FeasView F;
@@ -158,8 +162,7 @@ struct ScoreArgs {
     double *f_out, *h_out, *p95_out;
     uint8_t *sla_out, *feas_out;
     Sel sel;
-    int *error_flag;                // first error code (atomicCAS from 0)
-    long long *error_index;
+    unsigned long long *error_key;  // min over failing rows of (index << 8 | error code); ~0 = none
 };
 
 struct OracleArgs {

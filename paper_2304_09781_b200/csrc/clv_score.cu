@@ -330,80 +330,184 @@ cudaError_t launch_score_graphs(const ScoreArgs &a, const FamilyTables &T, int g
 }
 
 // ----------------------------------------------------------------- score_x
-// One THREAD per candidate: it walks its FleetConfig row (config id per GPU, then that
-// config's slices largest first, mig.py:240-242) and its variant bytes in order, adding
-// the exact integer rows.  Rows are read byte by byte through L1 (a candidate's bytes
-// are contiguous, so after the first touch of a 32-B sector the rest hit); slots are
-// processed four at a time so four variant loads are in flight per thread.
-__global__ void __launch_bounds__(SNT) score_x_kernel(const __grid_constant__ ScoreArgs a, int n) {
-    __shared__ ERow row[CLV_MAX_EDGES];
-    __shared__ double lat_by_rank[CLV_MAX_EDGES];
-    __shared__ unsigned char rank[CLV_MAX_EDGES];
-    __shared__ short row_of_id[256];
-    __shared__ unsigned char nsl[CLV_MAX_CONFIGS];
-    __shared__ unsigned char kinds[CLV_MAX_CONFIGS][8];
+// One thread per FleetConfig row, rows staged through shared memory a tile at a time.
+// Read straight from HBM, every byte load of a warp touched 32 different 64..500-B rows
+// (32 L1 wavefronts per load); here each warp copies its 32 rows of x^p with coalesced
+// byte loads into a padded layout (odd word stride: conflict-free column reads) and the
+// CTA copies the tile's x^v span (off[c0] .. off[c0 + rows]) with 16-B loads.  The walk
+// is flattened over the assignment slots -- one iteration per slot, the next GPU's
+// partition fetched by a single predicated refill (every partition has 1..7 slices,
+// mig.py:103-110) -- so lanes with 1-slice and 7-slice partitions do not serialise.
+// Sums are fp64 over exact integers (< 2^53: identical to the int64 sums), and the p95
+// term is the running max of lat95 over the slots (= lat_by_rank[top present rank]).
+//
+// Validation follows FleetConfig.__init__ (mig.py:248-263) then the SPEC's evaluation
+// (SPEC:267-275): an unknown partition id anywhere in the row -> InvalidConfigError;
+// else a length mismatch -> CarbonSchedError; else a variant < 1 -> CarbonSchedError;
+// else a variant > V or a memory-infeasible (variant, slice) -> InfeasibleAssignmentError.
+// Across candidates the LOWEST failing index is reported (a sequential loop raises at
+// the first bad row): one 64-bit atomicMin of (index << 8 | code).
+constexpr int XT = 128;                     // candidates (= threads) per tile
+constexpr int X_SMEM = 52 * 1024;           // dynamic staging bytes: x^p tile, then x^v span (4 CTAs / SM)
+
+struct __align__(16) XRow {
+    double thr, acc, en, idle, lat;
+    long long ok;                           // memory-feasible edge
+};
+
+template <bool XP_SMEM, bool XV_SMEM>
+__device__ __forceinline__ void walk_row(const uint8_t *xpr, const uint8_t *xvr, int mcnt, int n, int V,
+                                         const unsigned *cfg, const XRow *row, double &S0, double &S1,
+                                         double &S2, double &S3, double &lmax, int &err) {
+    // cfg[id]: bit 31 valid, bits 24..27 slice count (1..7), bits 0..20 slice kinds (3 bits each)
+    int g = 0, left = 0, bad_id = 0, lt1 = 0, infeas = 0, p = 0;
+    unsigned kw = 0;
+    for (; p < mcnt; ++p) {
+        if (left == 0) {
+            if (g == n) break;                         // more variants than slices
+            const unsigned c = cfg[XP_SMEM ? xpr[g] : __ldg(xpr + g)];
+            ++g;
+            if (!(c >> 31)) { bad_id = 1; break; }
+            left = (c >> 24) & 15; kw = c;
+        }
+        const int v = XV_SMEM ? xvr[p] : __ldg(xvr + p);
+        const int kind = kw & 7;
+        kw >>= 3; --left;
+        lt1 |= v == 0;
+        const bool vok = (unsigned)(v - 1) < (unsigned)V;
+        const XRow &R = row[vok ? (v - 1) * 5 + kind : 0];
+        infeas |= !vok || !R.ok;
+        S0 += R.thr; S1 += R.acc; S2 += R.en; S3 += R.idle;
+        lmax = R.lat > lmax ? R.lat : lmax;
+    }
+    // the rest of the partition row: every id must be known (InvalidConfigError comes
+    // first, mig.py:254) and its slices count towards the expected length
+    int expected = p + left;
+    for (; g < n && !bad_id; ++g) {
+        const unsigned c = cfg[XP_SMEM ? xpr[g] : __ldg(xpr + g)];
+        if (!(c >> 31)) bad_id = 1;
+        expected += (c >> 24) & 15;
+    }
+    err = bad_id ? CLV_ERR_INVALID_CONFIG
+        : expected != mcnt ? CLV_ERR_CARBON_SCHED
+        : lt1 ? SCORE_X_VARIANT_LT1
+        : infeas ? CLV_ERR_INFEASIBLE_ASSIGNMENT : 0;
+}
+
+__global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ ScoreArgs a, int n, int xp_stride,
+                                                     int xv_cap) {
+    __shared__ XRow row[CLV_MAX_EDGES];
+    __shared__ unsigned cfg[256];
+    extern __shared__ __align__(16) uint8_t xsm[];
+    // x^p rows at xp_stride (n padded to an odd number of words; 0 = n too large to stage)
+    uint8_t *sxp = xsm, *sxv = xsm + XT * xp_stride;
     const FamilyTables &T = *a.fam;
     const Topology &P = *a.topo;
-    stage_rows(row, lat_by_rank, rank, T);
-    for (int t = threadIdx.x; t < 256; t += SNT) row_of_id[t] = -1;
+    for (int e = threadIdx.x; e < CLV_MAX_EDGES; e += XT) {
+        const bool live = e < T.E;
+        row[e].thr = live ? (double)T.thr_q[e] : 0.0; row[e].acc = live ? (double)T.acc_q[e] : 0.0;
+        row[e].en = live ? (double)T.en_q[e] : 0.0; row[e].idle = live ? (double)T.idle_q[e % 5] : 0.0;
+        row[e].lat = live ? T.lat95[e] : 0.0;
+        row[e].ok = (live && ((T.mem_ok >> e) & 1ULL)) ? 1 : 0;
+    }
+    for (int t = threadIdx.x; t < 256; t += XT) cfg[t] = 0u;
     __syncthreads();
-    for (int r = threadIdx.x; r < P.K; r += SNT) {
-        if (P.ids[r] >= 0 && P.ids[r] < 256) row_of_id[P.ids[r]] = (short)r;
-        nsl[r] = (unsigned char)P.nslices[r];
-        for (int j = 0; j < 8; ++j) kinds[r][j] = P.kinds[r][j];
+    for (int r = threadIdx.x; r < P.K; r += XT) {
+        if (P.ids[r] >= 0 && P.ids[r] < 256 && P.nslices[r] >= 1 && P.nslices[r] <= 7) {
+            unsigned kw = 0;
+            for (int j = 0; j < P.nslices[r]; ++j) kw |= (unsigned)P.kinds[r][j] << (3 * j);
+            cfg[P.ids[r]] = 0x80000000u | ((unsigned)P.nslices[r] << 24) | kw;
+        }
     }
     __syncthreads();
     const int V = T.V;
-    const unsigned long long mem_ok = T.mem_ok;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     RecP r0 = recp_none(), r1 = recp_none();
     unsigned long long c_valid = 0, c_sla = 0;
-    for (long long c = (long long)blockIdx.x * SNT + threadIdx.x; c < a.count; c += (long long)gridDim.x * SNT) {
-        const uint8_t *xp = a.xp + c * n;
-        const long long off0 = __ldg(a.xv_off + c), off1 = __ldg(a.xv_off + c + 1);
-        const uint8_t *xv = a.xv + off0;
-        const long long mcnt = off1 - off0;
-        long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
-        unsigned long long m = 0;
-        int err = 0;
-        long long slot = 0;
-        for (int g = 0; g < n && !err; ++g) {
-            const int r = row_of_id[__ldg(xp + g)];
-            if (r < 0) { err = CLV_ERR_INVALID_CONFIG; break; }
-            const int ns = nsl[r];
-            if (slot + ns > mcnt) { err = CLV_ERR_CARBON_SCHED; break; }
-            int vv[7];
-#pragma unroll
-            for (int j = 0; j < 7; ++j) vv[j] = j < ns ? (int)__ldg(xv + slot + j) : 1;
-#pragma unroll
-            for (int j = 0; j < 7; ++j) {
-                if (j >= ns) break;
-                const int v = vv[j];
-                const int e = (v - 1) * 5 + kinds[r][j];
-                if (v < 1 || v > V || !((mem_ok >> e) & 1ULL)) { err = CLV_ERR_INFEASIBLE_ASSIGNMENT; break; }
-                S0 += row[e].thr; S1 += row[e].acc; S2 += row[e].en; S3 += row[e].idle;
-                m |= 1ULL << rank[e];
+    const long long ntiles = (a.count + XT - 1) / XT;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long c0 = tile * XT;
+        const int rows = (int)min((long long)XT, a.count - c0);
+        const long long G0 = __ldg(a.xv_off + c0), G1 = __ldg(a.xv_off + c0 + rows);
+        const bool xv_fits = (G1 - G0) + 16 <= xv_cap;
+        __syncthreads();                                   // previous tile's rows are consumed
+        if (xp_stride) {                                   // warp w copies rows 32w .. 32w + 31
+            const int r_end = min(32 * wid + 32, rows);
+            for (int r = 32 * wid; r < r_end; ++r) {
+                const uint8_t *g = a.xp + (c0 + r) * n;
+                for (int q = lane; q < n; q += 32) sxp[r * xp_stride + q] = __ldcs(g + q);
             }
-            slot += ns;
         }
-        if (!err && slot != mcnt) err = CLV_ERR_CARBON_SCHED;              // length mismatch
-        if (err) {
-            if (atomicCAS(a.error_flag, 0, err) == 0) *a.error_index = c;
-            if (a.sla_out) a.sla_out[c] = 0;
-        } else {
-            Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)], (double)mcnt, a.ec);
-            ++c_valid;
-            c_sla += sc.sla;
-            consider(r0, r1, sc, a.index_base + c, a.select_mode);
-            if (a.f_out) a.f_out[c] = sc.f;
-            if (a.h_out) a.h_out[c] = sc.h;
-            if (a.sla_out) a.sla_out[c] = sc.sla;
+        int lead = 0;
+        if (xv_fits) {
+            // sxv[k] holds the byte at (aligned-down address of xv + G0) + k; whole 16-B
+            // chunks inside [G0, G1) are vector loads, the partial head / tail chunks bytes
+            const uint8_t *g0 = a.xv + G0;
+            lead = (int)(reinterpret_cast<uintptr_t>(g0) & 15);
+            const uint8_t *ga = g0 - lead;
+            const long long len = G1 - G0;
+            const long long nch = (lead + len + 15) >> 4;
+            for (long long q = threadIdx.x; q < nch; q += XT) {
+                const long long lo = (q << 4) - lead;             // chunk bytes [lo, lo + 16) relative to G0
+                if (lo >= 0 && lo + 16 <= len) {
+                    reinterpret_cast<uint4 *>(sxv)[q] = __ldcs(reinterpret_cast<const uint4 *>(ga) + q);
+                } else {
+                    for (int b = 0; b < 16; ++b)
+                        if (lo + b >= 0 && lo + b < len) sxv[(q << 4) + b] = g0[lo + b];
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < rows) {
+            const long long c = c0 + threadIdx.x;
+            const long long o0 = __ldg(a.xv_off + c), o1 = __ldg(a.xv_off + c + 1);
+            double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, lmax = 0.0;
+            int err;
+            if (o1 - o0 < 0 || o1 - o0 > 0x7FFFFFFFLL) {
+                err = CLV_ERR_CARBON_SCHED;
+            } else {
+                const int mcnt = (int)(o1 - o0);
+                const uint8_t *sxr = sxv + lead + (o0 - G0), *gxr = a.xv + o0;
+                const uint8_t *sxpr = sxp + threadIdx.x * xp_stride, *gxpr = a.xp + c * n;
+                if (xp_stride && xv_fits)
+                    walk_row<true, true>(sxpr, sxr, mcnt, n, V, cfg, row, S0, S1, S2, S3, lmax, err);
+                else if (xp_stride)
+                    walk_row<true, false>(sxpr, gxr, mcnt, n, V, cfg, row, S0, S1, S2, S3, lmax, err);
+                else
+                    walk_row<false, false>(gxpr, gxr, mcnt, n, V, cfg, row, S0, S1, S2, S3, lmax, err);
+            }
+            if (err) {
+                atomicMin(a.error_key, ((unsigned long long)c << 8) | (unsigned)err);
+                if (a.sla_out) a.sla_out[c] = 0;
+            } else {
+                Score sc = epilogue_d(S0, S1, S2, S3, lmax, (double)(o1 - o0), a.ec);
+                ++c_valid;
+                c_sla += sc.sla;
+                consider(r0, r1, sc, a.index_base + c, a.select_mode);
+                if (a.f_out) a.f_out[c] = sc.f;
+                if (a.h_out) a.h_out[c] = sc.h;
+                if (a.sla_out) a.sla_out[c] = sc.sla;
+            }
         }
     }
-    grid_finish<SNT>(r0, r1, c_valid, c_sla, a.sel);
+    grid_finish<XT>(r0, r1, c_valid, c_sla, a.sel);
 }
 
-cudaError_t launch_score_x(const ScoreArgs &a, int n, int grid, cudaStream_t s) {
-    score_x_kernel<<<grid, SNT, 0, s>>>(a, n);
+cudaError_t launch_score_x(const ScoreArgs &a, int n, int max_grid, cudaStream_t s) {
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // n padded to whole words, the word count made odd (row r's word w sits in bank
+    // (r * stride / 4 + w) mod 32: distinct across a warp's rows)
+    const int stride = ((n + 3) & ~3) | 4;
+    const int xp_stride = (long long)XT * stride <= X_SMEM / 2 ? stride : 0;
+    const int xv_cap = X_SMEM - XT * xp_stride;
+    cudaError_t e = cudaFuncSetAttribute(score_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, X_SMEM);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score_x_kernel, XT, X_SMEM);
+    const long long tiles = (a.count + XT - 1) / XT;
+    const long long g = std::max(1LL, std::min({tiles, (long long)sms * std::max(occ, 1), (long long)max_grid}));
+    score_x_kernel<<<(unsigned)g, XT, X_SMEM, s>>>(a, n, xp_stride, xv_cap);
     return cudaGetLastError();
 }
 

@@ -109,6 +109,31 @@ def main():
         except errors.CarbonSchedError as exc:
             bad.append([p, a, type(exc).__name__])
     g["fleet_errors"] = bad
+    # error precedence of FleetConfig.__init__ on rows with several defects at once
+    # (own RNG so the fixtures above are unchanged)
+    r2 = random.Random(2304097810)
+    ids = list(topo.config_ids)
+    prec = []
+    for k in range(200):
+        n = r2.randint(1, 6)
+        p = [r2.choice(ids) for _ in range(n)]
+        m = sum(len(topo.config_slices(c)) for c in p)
+        a = [r2.randint(1, 7) for _ in range(m)]
+        if r2.random() < 0.3:
+            p[r2.randrange(n)] = r2.choice([0, 20, 42, 200])
+        if r2.random() < 0.3:
+            if a and r2.random() < 0.5:
+                a.pop(r2.randrange(len(a)))
+            else:
+                a.insert(r2.randrange(len(a) + 1), r2.randint(1, 7))
+        if a and r2.random() < 0.3:
+            a[r2.randrange(len(a))] = 0
+        try:
+            mig.FleetConfig(p, a)
+            prec.append([p, a, "ok"])
+        except errors.CarbonSchedError as exc:
+            prec.append([p, a, type(exc).__name__])
+    g["fleet_error_precedence"] = prec
     with open(OUT, "w") as fh:
         json.dump(g, fh, indent=0, sort_keys=True)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")

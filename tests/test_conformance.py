@@ -101,6 +101,27 @@ def test_fleet_config_golden():
             FleetConfig(p, a)
 
 
+CTOR_OUTCOME = {"invalid_config": "InvalidConfigError", "length": "CarbonSchedError",
+                "variant_lt1": "CarbonSchedError", "infeasible": "ok", None: "ok"}
+
+
+def test_fleet_error_precedence_golden():
+    """Rows with several defects: FleetConfig here and the oracle's fleet_row_error (the
+    checker of clv_score_x's error reporting) both follow the reference's order."""
+    from oracle.search import fleet_row_error
+    from oracle.tables import OracleTables
+    from paper_2304_09781_b200.profiles import synthetic_profile
+    T = OracleTables.from_profile(synthetic_profile("bert"))
+    for p, a, outcome in GOLDEN["fleet_error_precedence"]:
+        assert CTOR_OUTCOME[fleet_row_error(p, a, DEFAULT_TOPOLOGY, T)] == outcome, (p, a)
+        if outcome == "ok":
+            FleetConfig(p, a)
+        else:
+            with pytest.raises(errors.CarbonSchedError) as ei:
+                FleetConfig(p, a)
+            assert type(ei.value).__name__ == outcome
+
+
 def test_load_topology_roundtrip(tmp_path):
     path = tmp_path / "topo.json"
     path.write_text(json.dumps(DEFAULT_TOPOLOGY.to_json_dict()))

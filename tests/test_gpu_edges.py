@@ -144,3 +144,107 @@ def test_score_x_error_paths(engine):
         engine.score_x(*csr(good, lambda xp, xv: xv.__setitem__(0, xv[0][:-1])), 2, prof, sc)
     with pytest.raises(InfeasibleAssignmentError):
         engine.score_x(*csr(good, lambda xp, xv: xv[0].__setitem__(1, 6)), 2, prof, sc)
+
+
+def _score_rows(engine, prof, sc, rows, n):
+    xp = np.array([p for p, a in rows], dtype=np.uint8).reshape(len(rows), n)
+    xv = np.array([v for p, a in rows for v in a], dtype=np.uint8)
+    off = np.concatenate([[0], np.cumsum([len(a) for p, a in rows])]).astype(np.int64)
+    return engine.score_x(xp, xv, off, n, prof, sc)
+
+
+def test_score_x_error_precedence(engine):
+    """The reference's multi-defect rows (golden, FleetConfig.__init__ order), one at a time
+    and as batches: the reported row is the lowest failing index, its error the first in
+    the reference's order (unknown id, length, variant < 1), then the SPEC's infeasible
+    assignment."""
+    import json
+    import os
+    from oracle.search import fleet_row_error
+    from paper_2304_09781_b200 import errors as E
+    G = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_l0.json")))
+    prof = synthetic_profile("bert")
+    T = OracleTables.from_profile(prof)
+    EXC = {"invalid_config": E.InvalidConfigError, "length": E.CarbonSchedError,
+           "variant_lt1": E.CarbonSchedError, "infeasible": E.InfeasibleAssignmentError}
+    sc = {n: calibrate(prof, T, n, 300.0, 0.5) for n in range(1, 7)}
+    rows = [(p, a) for p, a, _ in G["fleet_error_precedence"]]
+    kinds = set()
+    for p, a in rows:
+        want = fleet_row_error(p, a, DEFAULT_TOPOLOGY, T)
+        kinds.add(want)
+        if want is None:
+            best, _ = _score_rows(engine, prof, sc[len(p)], [(p, a)], len(p))
+            assert best["valid_count"] == 1
+        else:
+            with pytest.raises(E.CarbonSchedError) as ei:
+                _score_rows(engine, prof, sc[len(p)], [(p, a)], len(p))
+            assert type(ei.value) is EXC[want], (p, a, want)
+            assert "candidate 0:" in str(ei.value)
+    assert kinds == {None, "invalid_config", "length", "variant_lt1", "infeasible"}
+    for n in range(1, 7):
+        batch = [r for r in rows if len(r[0]) == n]
+        errs = [fleet_row_error(p, a, DEFAULT_TOPOLOGY, T) for p, a in batch]
+        bad = [i for i, e in enumerate(errs) if e]
+        if not bad:
+            continue
+        with pytest.raises(E.CarbonSchedError) as ei:
+            _score_rows(engine, prof, sc[n], batch, n)
+        assert type(ei.value) is EXC[errs[bad[0]]]
+        assert "candidate %d:" % bad[0] in str(ei.value)
+
+
+def test_score_x_lowest_failing_index_large(engine):
+    """64-GPU rows, errors planted in many tiles: the lowest failing index wins."""
+    from oracle.search import draw_candidate, Pod
+    from paper_2304_09781_b200 import errors as E
+    prof = synthetic_profile("bert")
+    T = OracleTables.from_profile(prof)
+    n = 64
+    sc = calibrate(prof, T, n, 300.0, 0.5)
+    rows = [tuple(map(list, draw_candidate(5, i, [Pod(T, sc, n, 1.0)], DEFAULT_TOPOLOGY)[0])) for i in range(3000)]
+    best, _ = _score_rows(engine, prof, sc, rows, n)
+    assert best["valid_count"] == 3000
+    bad = [list(r) for r in rows]
+    bad[2900][0][5] = 42                                    # unknown id
+    bad[1777][1] = bad[1777][1][:-1]                        # length
+    bad[2222][1][3] = 0                                     # variant < 1
+    with pytest.raises(E.CarbonSchedError) as ei:
+        _score_rows(engine, prof, sc, [tuple(r) for r in bad], n)
+    assert type(ei.value) is E.CarbonSchedError and "candidate 1777:" in str(ei.value)
+    bad[1200][1][0] = 9                                     # variant > V
+    with pytest.raises(E.InfeasibleAssignmentError, match="candidate 1200:"):
+        _score_rows(engine, prof, sc, [tuple(r) for r in bad], n)
+
+
+@pytest.mark.parametrize("shape", ["wide_rows", "many_gpus"])
+def test_score_x_unstaged_paths(engine, shape):
+    """Tiles whose x^v span overflows the shared-memory stage (64 GPUs of 7 x 1g slices) and
+    fleets too wide for the x^p stage (n = 320) take the direct-load walk: same bits."""
+    from oracle.search import fleet_graph, row_kinds
+    from paper_2304_09781_b200.mig import FleetConfig
+    prof = synthetic_profile("efficientnet")
+    T = OracleTables.from_profile(prof)
+    rng = np.random.default_rng(11)
+    ids = list(DEFAULT_TOPOLOGY.config_ids)
+    one_g = max(ids, key=lambda c: len(DEFAULT_TOPOLOGY.config_slices(c)))
+    n = 64 if shape == "wide_rows" else 320
+    fleets = []
+    for i in range(700):
+        if shape == "wide_rows":
+            parts = [one_g if rng.random() < 0.9 else int(rng.choice(ids)) for _ in range(n)]
+        else:
+            parts = [int(rng.choice(ids)) for _ in range(n)]
+        m = sum(len(DEFAULT_TOPOLOGY.config_slices(c)) for c in parts)
+        fe = [[v for v in range(1, T.V + 1) if T.mem_ok[(v - 1) * 5 + k]] for k in range(5)]
+        kinds = [k for c in parts for k in row_kinds(DEFAULT_TOPOLOGY, c)]
+        assign = [int(rng.choice(fe[k])) for k in kinds]
+        assert len(assign) == m
+        fleets.append(FleetConfig(parts, assign))
+    sc = calibrate(prof, T, n, 300.0, 0.5)
+    best, outs = engine.score_fleets(fleets, prof, sc)
+    W = np.array([fleet_graph(f.partitions, f.assignments, DEFAULT_TOPOLOGY, T) for f in fleets])
+    ev = evaluate(W, T, sc)
+    assert bits_equal(outs["f"].cpu().numpy(), ev.f)
+    assert bits_equal(outs["h"].cpu().numpy(), ev.h)
+    assert best["index"] == select_best(ev.h, ev.sla)
