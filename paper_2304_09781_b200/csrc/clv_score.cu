@@ -338,8 +338,12 @@ cudaError_t launch_score_graphs(const ScoreArgs &a, const FamilyTables &T, int g
 // is flattened over the assignment slots -- one iteration per slot, the next GPU's
 // partition fetched by a single predicated refill (every partition has 1..7 slices,
 // mig.py:103-110) -- so lanes with 1-slice and 7-slice partitions do not serialise.
-// Sums are fp64 over exact integers (< 2^53: identical to the int64 sums), and the p95
-// term is the running max of lat95 over the slots (= lat_by_rank[top present rank]).
+// Per slot the thread only bumps its own 16-bit count of the (variant, slice) bucket
+// (counts laid out [bucket][thread]: conflict-free); the rows -- one 16-B int4 of the
+// fixed-point values, each < 2^31 -- are applied once per edge after the walk
+// (S = sum_e count_e * row_e, exact int64), which also yields the presence mask for
+// the p95 term and the memory-fit check.  Rows longer than 65,535 slots take the
+// direct per-slot sum.
 //
 // Validation follows FleetConfig.__init__ (mig.py:248-263) then the SPEC's evaluation
 // (SPEC:267-275): an unknown partition id anywhere in the row -> InvalidConfigError;
@@ -348,44 +352,64 @@ cudaError_t launch_score_graphs(const ScoreArgs &a, const FamilyTables &T, int g
 // Across candidates the LOWEST failing index is reported (a sequential loop raises at
 // the first bad row): one 64-bit atomicMin of (index << 8 | code).
 constexpr int XT = 128;                     // candidates (= threads) per tile
-constexpr int X_SMEM = 52 * 1024;           // dynamic staging bytes: x^p tile, then x^v span (4 CTAs / SM)
+constexpr int X_SMEM = 40 * 1024;           // dynamic staging bytes: x^p tile, then x^v span (4 CTAs / SM)
 
-struct __align__(16) XRow {
-    double thr, acc, en, idle, lat;
-    long long ok;                           // memory-feasible edge
-};
 
-template <bool XP_SMEM, bool XV_SMEM>
-__device__ __forceinline__ void walk_row(const uint8_t *xpr, const uint8_t *xvr, int mcnt, int n, int V,
-                                         const unsigned *cfg, const XRow *row, double &S0, double &S1,
-                                         double &S2, double &S3, double &lmax, int &err) {
-    // cfg[id]: bit 31 valid, bits 24..27 slice count (1..7), bits 0..20 slice kinds (3 bits each)
-    int g = 0, left = 0, bad_id = 0, lt1 = 0, infeas = 0, p = 0;
+template <bool XP_SMEM, bool XV_SMEM, bool HIST>
+__device__ __forceinline__ void walk_row(unsigned short *hc, const uint8_t *xpr, const uint8_t *xvr, int mcnt, int n,
+                                         int V, const unsigned *cfg, const int4 *row, const unsigned char *rank_ok,
+                                         long long &S0, long long &S1, long long &S2, long long &S3,
+                                         unsigned long long &m, int &err) {
+    // cfg[id]: bit 31 valid, bits 24..27 slice count (1..7), bits 0..20 slice kinds (3 bits each).
+    // HIST: slot counts per bucket b = min(v, V + 1) * 5 + kind -- bucket row 0 holds the
+    // variants < 1, rows 1..V the edges (v - 1) * 5 + kind, row V + 1 the variants > V --
+    // so the per-slot path has no checks at all.  A refill past the last GPU (more
+    // variants than slices) re-reads GPU n - 1: such a row is a length error anyway.
+    int g = 0, left = 0, bad_id = 0, lt1 = 0, infeas = 0, expected = 0;
     unsigned kw = 0;
-    for (; p < mcnt; ++p) {
+    for (int p = 0; p < mcnt; ++p) {
         if (left == 0) {
-            if (g == n) break;                         // more variants than slices
-            const unsigned c = cfg[XP_SMEM ? xpr[g] : __ldg(xpr + g)];
-            ++g;
-            if (!(c >> 31)) { bad_id = 1; break; }
-            left = (c >> 24) & 15; kw = c;
+            const unsigned c = cfg[XP_SMEM ? xpr[min(g, n - 1)] : __ldg(xpr + min(g, n - 1))];
+            const int ns = (c >> 24) & 15;                 // 0 for an unknown id
+            bad_id |= !(c >> 31);
+            expected += g < n ? ns : 0;
+            left = ns > 0 ? ns : 1;
+            kw = c; ++g;
         }
         const int v = XV_SMEM ? xvr[p] : __ldg(xvr + p);
         const int kind = kw & 7;
         kw >>= 3; --left;
-        lt1 |= v == 0;
-        const bool vok = (unsigned)(v - 1) < (unsigned)V;
-        const XRow &R = row[vok ? (v - 1) * 5 + kind : 0];
-        infeas |= !vok || !R.ok;
-        S0 += R.thr; S1 += R.acc; S2 += R.en; S3 += R.idle;
-        lmax = R.lat > lmax ? R.lat : lmax;
+        if (HIST) {
+            hc[(min(v, V + 1) * 5 + kind) * XT] += 1;
+        } else {
+            lt1 |= v == 0;
+            const bool vok = (unsigned)(v - 1) < (unsigned)V;
+            const int e = vok ? (v - 1) * 5 + kind : 0;
+            const int4 R = row[e];
+            const unsigned ro = rank_ok[e];
+            infeas |= !vok || !ro;
+            S0 += R.x; S1 += R.y; S2 += R.z; S3 += R.w;
+            m |= 1ULL << (ro & 63);
+        }
+    }
+    if (HIST) {                                        // apply the rows; leave the counts zeroed
+        const int NB = 5 * (V + 2);
+        for (int b = 0; b < NB; ++b) {
+            const unsigned c = hc[b * XT];
+            hc[b * XT] = 0;
+            if (b < 5) { lt1 |= c != 0; continue; }
+            if (b >= 5 * (V + 1)) { infeas |= c != 0; continue; }
+            const int4 R = row[b - 5];
+            const unsigned ro = rank_ok[b - 5];
+            S0 += (long long)c * R.x; S1 += (long long)c * R.y; S2 += (long long)c * R.z; S3 += (long long)c * R.w;
+            if (c) { m |= 1ULL << (ro & 63); infeas |= !ro; }
+        }
     }
     // the rest of the partition row: every id must be known (InvalidConfigError comes
     // first, mig.py:254) and its slices count towards the expected length
-    int expected = p + left;
-    for (; g < n && !bad_id; ++g) {
+    for (; g < n; ++g) {
         const unsigned c = cfg[XP_SMEM ? xpr[g] : __ldg(xpr + g)];
-        if (!(c >> 31)) bad_id = 1;
+        bad_id |= !(c >> 31);
         expected += (c >> 24) & 15;
     }
     err = bad_id ? CLV_ERR_INVALID_CONFIG
@@ -396,8 +420,11 @@ __device__ __forceinline__ void walk_row(const uint8_t *xpr, const uint8_t *xvr,
 
 __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ ScoreArgs a, int n, int xp_stride,
                                                      int xv_cap) {
-    __shared__ XRow row[CLV_MAX_EDGES];
+    __shared__ int4 row[CLV_MAX_EDGES];
+    __shared__ double lat_by_rank[CLV_MAX_EDGES];
+    __shared__ unsigned char rank_ok[CLV_MAX_EDGES];   // 0x40 | rank when memory-feasible, else 0
     __shared__ unsigned cfg[256];
+    __shared__ unsigned short hist[(CLV_MAX_EDGES + 10) * XT];  // [bucket][thread] slot counts of the row
     extern __shared__ __align__(16) uint8_t xsm[];
     // x^p rows at xp_stride (n padded to an odd number of words; 0 = n too large to stage)
     uint8_t *sxp = xsm, *sxv = xsm + XT * xp_stride;
@@ -405,12 +432,13 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
     const Topology &P = *a.topo;
     for (int e = threadIdx.x; e < CLV_MAX_EDGES; e += XT) {
         const bool live = e < T.E;
-        row[e].thr = live ? (double)T.thr_q[e] : 0.0; row[e].acc = live ? (double)T.acc_q[e] : 0.0;
-        row[e].en = live ? (double)T.en_q[e] : 0.0; row[e].idle = live ? (double)T.idle_q[e % 5] : 0.0;
-        row[e].lat = live ? T.lat95[e] : 0.0;
-        row[e].ok = (live && ((T.mem_ok >> e) & 1ULL)) ? 1 : 0;
+        row[e] = live ? make_int4((int)T.thr_q[e], (int)T.acc_q[e], (int)T.en_q[e], (int)T.idle_q[e % 5])
+                      : make_int4(0, 0, 0, 0);
+        lat_by_rank[e] = live ? T.lat_by_rank[e] : 0.0;
+        rank_ok[e] = (live && ((T.mem_ok >> e) & 1ULL)) ? (unsigned char)(0x40 | T.rank[e]) : 0;
     }
     for (int t = threadIdx.x; t < 256; t += XT) cfg[t] = 0u;
+    for (int q = threadIdx.x; q < (CLV_MAX_EDGES + 10) * XT; q += XT) hist[q] = 0;
     __syncthreads();
     for (int r = threadIdx.x; r < P.K; r += XT) {
         if (P.ids[r] >= 0 && P.ids[r] < 256 && P.nslices[r] >= 1 && P.nslices[r] <= 7) {
@@ -461,7 +489,8 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
         if (threadIdx.x < rows) {
             const long long c = c0 + threadIdx.x;
             const long long o0 = __ldg(a.xv_off + c), o1 = __ldg(a.xv_off + c + 1);
-            double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, lmax = 0.0;
+            long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+            unsigned long long m = 0;
             int err;
             if (o1 - o0 < 0 || o1 - o0 > 0x7FFFFFFFLL) {
                 err = CLV_ERR_CARBON_SCHED;
@@ -469,18 +498,21 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
                 const int mcnt = (int)(o1 - o0);
                 const uint8_t *sxr = sxv + lead + (o0 - G0), *gxr = a.xv + o0;
                 const uint8_t *sxpr = sxp + threadIdx.x * xp_stride, *gxpr = a.xp + c * n;
-                if (xp_stride && xv_fits)
-                    walk_row<true, true>(sxpr, sxr, mcnt, n, V, cfg, row, S0, S1, S2, S3, lmax, err);
+                unsigned short *hc = hist + threadIdx.x;
+                if (mcnt > 0xFFFF)
+                    walk_row<false, false, false>(hc, gxpr, gxr, mcnt, n, V, cfg, row, rank_ok, S0, S1, S2, S3, m, err);
+                else if (xp_stride && xv_fits)
+                    walk_row<true, true, true>(hc, sxpr, sxr, mcnt, n, V, cfg, row, rank_ok, S0, S1, S2, S3, m, err);
                 else if (xp_stride)
-                    walk_row<true, false>(sxpr, gxr, mcnt, n, V, cfg, row, S0, S1, S2, S3, lmax, err);
+                    walk_row<true, false, true>(hc, sxpr, gxr, mcnt, n, V, cfg, row, rank_ok, S0, S1, S2, S3, m, err);
                 else
-                    walk_row<false, false>(gxpr, gxr, mcnt, n, V, cfg, row, S0, S1, S2, S3, lmax, err);
+                    walk_row<false, false, true>(hc, gxpr, gxr, mcnt, n, V, cfg, row, rank_ok, S0, S1, S2, S3, m, err);
             }
             if (err) {
                 atomicMin(a.error_key, ((unsigned long long)c << 8) | (unsigned)err);
                 if (a.sla_out) a.sla_out[c] = 0;
             } else {
-                Score sc = epilogue_d(S0, S1, S2, S3, lmax, (double)(o1 - o0), a.ec);
+                Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)], (double)(o1 - o0), a.ec);
                 ++c_valid;
                 c_sla += sc.sla;
                 consider(r0, r1, sc, a.index_base + c, a.select_mode);

@@ -217,10 +217,11 @@ def test_score_x_lowest_failing_index_large(engine):
         _score_rows(engine, prof, sc, [tuple(r) for r in bad], n)
 
 
-@pytest.mark.parametrize("shape", ["wide_rows", "many_gpus"])
+@pytest.mark.parametrize("shape", ["wide_rows", "many_gpus", "huge_rows"])
 def test_score_x_unstaged_paths(engine, shape):
-    """Tiles whose x^v span overflows the shared-memory stage (64 GPUs of 7 x 1g slices) and
-    fleets too wide for the x^p stage (n = 320) take the direct-load walk: same bits."""
+    """Tiles whose x^v span overflows the shared-memory stage (64 GPUs of 7 x 1g slices),
+    fleets too wide for the x^p stage (n = 320) and rows past the 16-bit slot counters
+    (n = 9,500, > 65,535 slots) take the direct-load / direct-sum walks: same bits."""
     from oracle.search import fleet_graph, row_kinds
     from paper_2304_09781_b200.mig import FleetConfig
     prof = synthetic_profile("efficientnet")
@@ -228,10 +229,10 @@ def test_score_x_unstaged_paths(engine, shape):
     rng = np.random.default_rng(11)
     ids = list(DEFAULT_TOPOLOGY.config_ids)
     one_g = max(ids, key=lambda c: len(DEFAULT_TOPOLOGY.config_slices(c)))
-    n = 64 if shape == "wide_rows" else 320
+    n = {"wide_rows": 64, "many_gpus": 320, "huge_rows": 9500}[shape]
     fleets = []
-    for i in range(700):
-        if shape == "wide_rows":
+    for i in range(700 if shape != "huge_rows" else 6):
+        if shape != "many_gpus":
             parts = [one_g if rng.random() < 0.9 else int(rng.choice(ids)) for _ in range(n)]
         else:
             parts = [int(rng.choice(ids)) for _ in range(n)]
