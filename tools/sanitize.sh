@@ -14,6 +14,16 @@ for mode in ("best","uniform"):
 b=eng.anneal(st,prof,sc,AnnealParams(max_steps=3, proposal="uniform", evaluate="proposal"),1,cluster=3)
 best,_=eng.score_graphs(st,prof,sc)
 eng.oracle_search(prof, eng.calibrate(prof,1,400.0,0.5))
+import numpy as np
+from paper_2304_09781_b200.search import random_fleets
+fl=random_fleets(eng,prof,64,9,300,0)
+eng.score_fleets(fl,prof,sc)
+for f in (fl[:5],):
+    xp=np.array([x.partitions for x in f],dtype=np.uint8); xvs=[np.array(x.assignments,dtype=np.uint8) for x in f]
+    xvs[3]=xvs[3][:-2]; xp[4,7]=99
+    off=np.concatenate([[0],np.cumsum([len(x) for x in xvs])]).astype(np.int64)
+    try: eng.score_x(xp,np.concatenate(xvs),off,64,prof,sc)
+    except Exception as e: print("expected:", type(e).__name__, e)
 torch.cuda.synchronize(); print("ok")'
 for tool in memcheck racecheck synccheck; do
   echo "== $tool"
