@@ -235,13 +235,17 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
     // Feasibility of the 650 slice deltas, 3 per thread, as two batched round trips:
     // all rectangle offsets first, then all bitset words (feasible() in clv_common.cuh
     // would serialise the 2 dependent loads of each lookup).
+    // Warps 1.. only (3 deltas per thread): warp 0 builds the present-edge list below
+    // meanwhile, so the two round trips are off its path.
+    constexpr int FT = ANT - 32;
+    static_assert(3 * FT >= 650, "feasibility refresh needs 650 lookups");
     bool fres[3] = {false, false, false};
-    if (refresh) {                                 // uniform across the CTA
+    if (refresh && wid > 0) {                      // uniform across the CTA
         uint32_t obase[3], wofs[3], bit[3];
         bool cand[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-            const int t = threadIdx.x + q * ANT;
+            const int t = threadIdx.x - 32 + q * FT;
             int v[CLV_K];
 #pragma unroll
             for (int k = 0; k < CLV_K; ++k) v[k] = s.svec[k];
@@ -273,6 +277,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
     //     prefix of the removal pairs that start at it: (e_i, e_i) when w >= 2, then
     //     (e_i, e_j) for j > i -- i.e. the available pairs in ascending P(x, y), the
     //     same deterministic order in every CTA of the cluster.
+    const long long ptR = PROF ? clock64() : 0;
     if (wid == 0) {
         int k = 0;
         for (int e0 = 0; e0 < E; e0 += 32) {
@@ -299,6 +304,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
         if (lane == 0) { s.nPE = k; s.pfx[k] = pb; s.nRP = pb; }
     }
     __syncthreads();
+    const long long ptA = PROF ? clock64() : 0;
     // (2) every thread: a contiguous run of <= PER available pairs, their move-list
     //     lengths, and a block exclusive scan of the lengths in pair order.
     const int k = s.nPE, npairs = s.nRP;
@@ -334,6 +340,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
     }
     if (lane == 31) s.warp_len[wid] = il;
     __syncthreads();
+    const long long ptB = PROF ? clock64() : 0;
     if (threadIdx.x < 32) {
         const int l = lane < NWARP ? s.warp_len[lane] : 0;
         int l2 = l;
@@ -385,16 +392,19 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             r.r1 = (unsigned char)e; r.r2 = 0xFF; r.offm = 0; r.end = 0; r.pre = 0;
         }
     }
-    if (refresh) {
+    if (refresh && wid > 0) {
         for (int q = 0; q < 3; ++q) {
-            const int t = threadIdx.x + q * ANT;
+            const int t = threadIdx.x - 32 + q * FT;
             if (t < 25) s.feasS[t] = fres[q];
             else if (t < 650) s.feasD[t - 25] = fres[q];
         }
-        if (threadIdx.x < CLV_K) s.fsvec[threadIdx.x] = s.svec[threadIdx.x];
+        if (threadIdx.x - 32 < CLV_K) s.fsvec[threadIdx.x - 32] = s.svec[threadIdx.x - 32];
     }
     __syncthreads();
-    if (PROF && threadIdx.x == 0) { pacc[10] += pt1 - pt0; pacc[11] += clock64() - pt1; }
+    if (PROF && threadIdx.x == 0) {
+        pacc[10] += pt1 - pt0; pacc[11] += clock64() - pt1;
+        pacc[12] += ptA - pt0; pacc[13] += ptB - ptA; pacc[14] += pt1 - ptB; pacc[15] += ptR - pt0;
+    }
 }
 
 // Exact score of one neighbour folded into the thread's records.

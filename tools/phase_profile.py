@@ -19,7 +19,7 @@ from paper_2304_09781_b200.engine import CloverEngine  # noqa: E402
 from paper_2304_09781_b200.objective import AnnealParams  # noqa: E402
 from paper_2304_09781_b200.profiles import synthetic_profile  # noqa: E402
 
-SLOTS = 12
+SLOTS = 16
 NAMES = ["prepare", "score", "cta_reduce", "sync1", "leader", "sync2", "apply"]
 
 eng = CloverEngine(n_max=64)
@@ -45,6 +45,9 @@ print("cluster %d cycles/step leader CTA: %s\n  rank-1 CTA: %s" % (cl, lead, oth
 print("leader: apply_move %d cycles per step" % per_step(buf[:, 0, 9]))
 print("prepare: refresh + pair count + scans %d, entry build + singles %d cycles per step"
       % (per_step(buf[:, 0, 10]), per_step(buf[:, 0, 11])))
+print("prepare part 1: refresh + present-edge list + pair prefix %d | pair decode + thread scan %d | warp scan %d"
+      % (per_step(buf[:, 0, 12]), per_step(buf[:, 0, 13]), per_step(buf[:, 0, 14])))
+print("  of which thread 0 until the present-edge list starts (refresh issue / wait) %d" % per_step(buf[:, 0, 15]))
 print("feasibility refresh in %.1f%% of steps; prepare cycles per refresh step %d, per other step %d"
       % (100.0 * nref / steps.sum(), buf[:, 0, 7].sum() / max(nref, 1),
          (buf[:, 0, 0].sum() - buf[:, 0, 7].sum()) / max(steps.sum() - nref, 1)))
