@@ -181,6 +181,13 @@ int clv_score_graphs(clv_ctx *ctx, int family, const uint16_t *w_dev, int64_t co
                      int64_t index_base, const clv_eval_params *params, int select_mode,
                      double *f_dev, double *h_dev, uint8_t *sla_dev, uint8_t *feasible_dev,
                      double *p95_dev, clv_best *best, void *stream);
+/* clv_score_x: rows of n partition ids (xp, uint8[count][n]) and CSR variant bytes
+ * (xv, row c = xv[xv_offsets[c] .. xv_offsets[c+1])).  Row validation follows
+ * FleetConfig.__init__ (mig.py:248-263), then evaluation: an unknown partition id ->
+ * CLV_ERR_INVALID_CONFIG; else a length mismatch or a variant < 1 ->
+ * CLV_ERR_CARBON_SCHED; else a variant > V or one that does not fit its slice ->
+ * CLV_ERR_INFEASIBLE_ASSIGNMENT.  The error reported is that of the LOWEST failing
+ * row (its index in the message), as a sequential loop would raise it. */
 int clv_score_x(clv_ctx *ctx, int family, int n, const uint8_t *xp_dev,
                 const uint8_t *xv_dev, const int64_t *xv_offsets_dev, int64_t count,
                 int64_t index_base, const clv_eval_params *params, int select_mode,
