@@ -188,6 +188,18 @@ def _cpu_setup(scenario_tuple):
     _CPU["feas"] = FeasOracle(DEFAULT_TOPOLOGY, N_FLEET)
 
 
+def cpu_model():
+    """Host CPU model (report the core count and the lscpu model)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(starts, seed, max_steps, seconds):
     """Oracle port on one host core over a bounded sample of the same chains."""
     _cpu_setup(None)
@@ -199,7 +211,7 @@ def cpu_baseline(starts, seed, max_steps, seconds):
         chains += 1
         if spent >= seconds:
             break
-    return {"value": evals / spent, "unit": UNIT, "cores": 1, "kind": "port",
+    return {"value": evals / spent, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
             "sample": "%d of the step-0 chains (n=%d, V=7) annealed to termination by oracle/anneal.py, "
                       "%d candidates in %.1f s" % (chains, N_FLEET, evals, spent)}
 
@@ -230,7 +242,7 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": 1000.0 * total_time / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": _config(args, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                              "sample": "%d chains per step (one per core), n=%d, V=7, oracle/anneal.py" % (cores, N_FLEET)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
