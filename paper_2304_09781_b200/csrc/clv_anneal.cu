@@ -420,7 +420,7 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args
     // one evaluation scenario for every chain: its constants are kernel parameters
     // (constant-bank operands); per-chain scenarios come from the CTA's shared copy
     Score sc;
-    if constexpr (EC1) sc = epilogue_d(t, ac, en, id, lmax, mcnt, args.ec0);
+    if constexpr (EC1) sc = epilogue_t<true>(t, ac, en, id, lmax, mcnt, args.ec0);
     else sc = epilogue_d(t, ac, en, id, lmax, mcnt, s.ec);
     const unsigned long long key = okey(sc.h);
     if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; } }
@@ -760,7 +760,10 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
 
 template <int MODE, int MINB, int UNR, bool PROF = false>
 static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
-    auto kern = a.n_ec == 1 ? anneal_kernel<MODE, MINB, UNR, PROF, true> : anneal_kernel<MODE, MINB, UNR, PROF, false>;
+    // EC1: one scenario for every chain (constants as kernel parameters) whose ranges
+    // keep the branch-free divisions exact (fast_div_safe); else the general path
+    auto kern = (a.n_ec == 1 && a.fast_div) ? anneal_kernel<MODE, MINB, UNR, PROF, true>
+                                            : anneal_kernel<MODE, MINB, UNR, PROF, false>;
     const size_t smem = sizeof(AnnealSmem) + sizeof(RemEnt) * (size_t)(a.E * (a.E + 1) / 2);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
