@@ -412,6 +412,7 @@ int clv_score_graphs(clv_ctx *ctx, int family, const uint16_t *w_dev, int64_t co
     a.count = count; a.index_base = index_base; a.w = w_dev; a.topo = ctx->topo_dev;
     a.f_out = f_dev; a.h_out = h_dev; a.p95_out = p95_dev; a.sla_out = sla_dev; a.feas_out = feas_dev;
     a.sel = make_sel(ctx);
+    a.fast = fast_div_safe(a.ec, ctx->fam[family].lat95, ctx->fam[family].E) ? 1 : 0;
     CLV_CUDA(launch_score_graphs(a, ctx->fam[family], grid_for(ctx, count, 256), st), "score_graphs");
     if (!best) return CLV_OK;
     return fetch_best(ctx, select_mode, st, best);
@@ -434,6 +435,7 @@ int clv_score_x(clv_ctx *ctx, int family, int n, const uint8_t *xp_dev, const ui
     a.xp = xp_dev; a.xv = xv_dev; a.xv_off = xv_off_dev; a.topo = ctx->topo_dev;
     a.f_out = f_dev; a.h_out = h_dev; a.sla_out = sla_dev; a.sel = make_sel(ctx);
     a.error_key = reinterpret_cast<unsigned long long *>(ctx->err_index);
+    a.fast = fast_div_safe(a.ec, ctx->fam[family].lat95, ctx->fam[family].E) ? 1 : 0;
     CLV_CUDA(launch_score_x(a, n, grid_for(ctx, count, 256), st), "score_x");
     CLV_CUDA(cudaMemcpyAsync(ctx->host_err + 2, ctx->err_index, sizeof(long long), cudaMemcpyDeviceToHost, st), "copy err key");
     rc = fetch_best(ctx, select_mode, st, best);
@@ -519,6 +521,7 @@ int clv_oracle_search(clv_ctx *ctx, int family, int n, int64_t begin, int64_t en
     CLV_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
     a.fam = ctx->fam_dev + family; a.topo = ctx->topo_dev; a.begin = begin; a.end = end; a.n = n;
     a.sel = make_sel(ctx);
+    a.fast = fast_div_safe(a.ec, ctx->fam[family].lat95, ctx->fam[family].E) ? 1 : 0;
     CLV_CUDA(launch_oracle(a, grid_for(ctx, end - begin, 256), st), "oracle");
     return fetch_best(ctx, CLV_SELECT_ORACLE, st, best);
 }
@@ -637,6 +640,11 @@ int clv_sweep(clv_ctx *ctx, int n_pods, const clv_pod *pods, int64_t begin, int6
     CLV_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
     a.fam = ctx->fam_dev; a.topo = ctx->topo_dev; a.begin = begin; a.end = end; a.seed = seed;
     a.f_out = f_dev; a.h_out = h_dev; a.sla_out = sla_dev; a.sel = make_sel(ctx);
+    a.fast = 1;
+    for (int p = 0; p < a.n_pods; ++p) {
+        const FamilyTables &T = ctx->fam[a.pods[p].family];
+        if (!fast_div_safe(a.pods[p].ec, T.lat95, T.E)) a.fast = 0;
+    }
     CLV_CUDA(launch_sweep(a, grid_for(ctx, end - begin, 256), st), "sweep");
     if (!best) return CLV_OK;
     return fetch_best(ctx, CLV_SELECT_BEST_H, st, best);

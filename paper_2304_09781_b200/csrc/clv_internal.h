@@ -164,6 +164,7 @@ struct ScoreArgs {
     uint8_t *sla_out, *feas_out;
     Sel sel;
     unsigned long long *error_key;  // min over failing rows of (index << 8 | error code); ~0 = none
+    int fast;                       // ec and the family's lat95 satisfy fast_div_safe()
 };
 
 struct OracleArgs {
@@ -175,6 +176,7 @@ struct OracleArgs {
     long long row_off[CLV_MAX_CONFIGS + 1];
     int row_place[CLV_MAX_CONFIGS][8];   // mixed-radix place values per slice
     Sel sel;
+    int fast;                            // fast_div_safe(ec, family lat95)
 };
 
 struct SweepPod {
@@ -193,6 +195,7 @@ struct SweepArgs {
     double *f_out, *h_out;
     uint8_t *sla_out;
     Sel sel;
+    int fast;                        // every pod satisfies fast_div_safe()
 };
 
 cudaError_t launch_feas_level(uint32_t *bits, const uint32_t *off, int N, int bdim, int cdim,

@@ -165,7 +165,7 @@ struct GraphRows {
 // The p95 of a graph is the largest lat95 over its present edges: the present-edge
 // mask is split into 7-bit chunks and each chunk's maximum comes from a 128-entry
 // table (shared memory), so the per-edge work is one predicate-set bit.
-template <int V>
+template <int V, bool FAST>
 __global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_constant__ ScoreArgs a,
                                                                const __grid_constant__ GraphRows R) {
     constexpr int E = V * CLV_K;
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_cons
             const bool feas = !(pe[c] & R.bad) && pe[c] != 0 &&
                               feasible(a.F, n, sv[c][0], sv[c][1], sv[c][2], sv[c][3], sv[c][4]);
             if (feas) {
-                Score sc = epilogue_d(S0[c], S1[c], S2[c], S3, lmax,
+                Score sc = epilogue_t<FAST>(S0[c], S1[c], S2[c], S3, lmax,
                                       (double)(sv[c][0] + sv[c][1] + sv[c][2] + sv[c][3] + sv[c][4]), a.ec);
                 ++c_valid;
                 c_sla += sc.sla;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_cons
 
 template <int V>
 static cudaError_t launch_tma(const ScoreArgs &a, const GraphRows &R, cudaStream_t s) {
-    auto kern = score_graphs_tma_kernel<V>;
+    auto kern = a.fast ? score_graphs_tma_kernel<V, true> : score_graphs_tma_kernel<V, false>;
     const size_t smem = (size_t)GS * GT * V * CLV_K * 2;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -418,6 +418,7 @@ __device__ __forceinline__ void walk_row(unsigned short *hc, const uint8_t *xpr,
         : infeas ? CLV_ERR_INFEASIBLE_ASSIGNMENT : 0;
 }
 
+template <bool FAST>
 __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ ScoreArgs a, int n, int xp_stride,
                                                      int xv_cap) {
     __shared__ int4 row[CLV_MAX_EDGES];
@@ -512,7 +513,8 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
                 atomicMin(a.error_key, ((unsigned long long)c << 8) | (unsigned)err);
                 if (a.sla_out) a.sla_out[c] = 0;
             } else {
-                Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)], (double)(o1 - o0), a.ec);
+                Score sc = epilogue_t<FAST>((double)S0, (double)S1, (double)S2, (double)S3,
+                                            lat_by_rank[63 - __clzll((long long)m)], (double)(o1 - o0), a.ec);
                 ++c_valid;
                 c_sla += sc.sla;
                 consider(r0, r1, sc, a.index_base + c, a.select_mode);
@@ -534,16 +536,18 @@ cudaError_t launch_score_x(const ScoreArgs &a, int n, int max_grid, cudaStream_t
     const int stride = ((n + 3) & ~3) | 4;
     const int xp_stride = (long long)XT * stride <= X_SMEM / 2 ? stride : 0;
     const int xv_cap = X_SMEM - XT * xp_stride;
-    cudaError_t e = cudaFuncSetAttribute(score_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, X_SMEM);
+    auto kern = a.fast ? score_x_kernel<true> : score_x_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, X_SMEM);
     if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score_x_kernel, XT, X_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, XT, X_SMEM);
     const long long tiles = (a.count + XT - 1) / XT;
     const long long g = std::max(1LL, std::min({tiles, (long long)sms * std::max(occ, 1), (long long)max_grid}));
-    score_x_kernel<<<(unsigned)g, XT, X_SMEM, s>>>(a, n, xp_stride, xv_cap);
+    kern<<<(unsigned)g, XT, X_SMEM, s>>>(a, n, xp_stride, xv_cap);
     return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ oracle
+template <bool FAST>
 __global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ OracleArgs a) {
     __shared__ ERow row[CLV_MAX_EDGES];
     __shared__ double lat_by_rank[CLV_MAX_EDGES];
@@ -575,8 +579,8 @@ __global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ Ora
             S0 += row[e].thr; S1 += row[e].acc; S2 += row[e].en; S3 += row[e].idle;
             m |= 1ULL << rank[e];
         }
-        Score sc = epilogue(S0 * n, S1 * n, S2 * n, S3 * n, lat_by_rank[63 - __clzll((long long)m)],
-                            (double)(n * ns), a.ec);
+        Score sc = epilogue_t<FAST>((double)(S0 * n), (double)(S1 * n), (double)(S2 * n), (double)(S3 * n),
+                                    lat_by_rank[63 - __clzll((long long)m)], (double)(n * ns), a.ec);
         ++c_valid;
         c_sla += sc.sla;
         consider(r0, r1, sc, i, CLV_SELECT_ORACLE);
@@ -585,7 +589,8 @@ __global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ Ora
 }
 
 cudaError_t launch_oracle(const OracleArgs &a, int grid, cudaStream_t s) {
-    oracle_kernel<<<grid, SNT, 0, s>>>(a);
+    if (a.fast) oracle_kernel<true><<<grid, SNT, 0, s>>>(a);
+    else oracle_kernel<false><<<grid, SNT, 0, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -620,6 +625,7 @@ struct __align__(32) SRow {
 
 constexpr int ZROW = CLV_MAX_EDGES;           // all-zero row: a configuration draw adds nothing
 
+template <bool FAST>
 __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ SweepArgs a) {
     __shared__ SRow row[CLV_MAX_PODS][CLV_MAX_EDGES + 1];
     __shared__ unsigned long long rbit[CLV_MAX_PODS][CLV_MAX_EDGES + 1];
@@ -685,7 +691,7 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
                 g += cfg ? 1 : 0;
                 inst += cfg ? 0 : 1;
             }
-            Score sc = epilogue_d(S0, S1, S2, S3, lat_by_rank[p][63 - __clzll((long long)m)], (double)inst,
+            Score sc = epilogue_t<FAST>(S0, S1, S2, S3, lat_by_rank[p][63 - __clzll((long long)m)], (double)inst,
                                   a.pods[p].ec);
             const double wt = a.pods[p].weight;
             if (p == 0) { f = wt * sc.f; h = wt * sc.h; }
@@ -706,7 +712,8 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
 }
 
 cudaError_t launch_sweep(const SweepArgs &a, int grid, cudaStream_t s) {
-    sweep_kernel<<<grid, SNT, 0, s>>>(a);
+    if (a.fast) sweep_kernel<true><<<grid, SNT, 0, s>>>(a);
+    else sweep_kernel<false><<<grid, SNT, 0, s>>>(a);
     return cudaGetLastError();
 }
 
