@@ -205,6 +205,17 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
                clv_log_row *log_dev, void *stream);
 int clv_select_chains(clv_ctx *ctx, const clv_chain_result *results_dev, int n_chains,
                       int64_t chain_base, clv_record *record_dev, void *stream);
+/* clv_replan: one complete re-plan from HOST buffers in one call -- start graphs copied
+ * H2D, clv_anneal, clv_select_chains, every output copied D2H, stream synchronised.
+ * Device staging is context-owned; host buffers should be pinned for async copies.
+ * Replaces the reference-side loop over independent anneal() runs
+ * plus its best tracking for one GPU; multi-rank callers exchange the
+ * returned record (clv_reduce_records). */
+int clv_replan(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base,
+               const uint16_t *start_w_host, const clv_eval_params *params, int n_params,
+               const clv_anneal_params *ap, uint64_t seed, int cluster_size,
+               clv_chain_result *results_host, uint16_t *best_w_host, uint16_t *final_w_host,
+               clv_record *record_host, void *stream);
 int clv_reduce_records(clv_ctx *ctx, const clv_record *records_dev, int count,
                        clv_record *out_dev, void *stream);
 int clv_sweep(clv_ctx *ctx, int n_pods, const clv_pod *pods, int64_t begin, int64_t end,

@@ -100,6 +100,8 @@ SIGNATURES = {
     "clv_anneal": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_i32, ctypes.POINTER(AnnealParamsC),
                            c_u64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "clv_select_chains": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "clv_replan": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_i32, ctypes.POINTER(AnnealParamsC),
+                           c_u64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "clv_reduce_records": (c_i32, [c_vp, c_vp, c_i32, c_vp, c_vp]),
     "clv_sweep": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_i64, c_u64, c_vp, c_vp, c_vp, ctypes.POINTER(Best), c_vp]),
     "clv_sweep_decode": (c_i32, [c_vp, c_i32, c_vp, c_u64, c_i64, c_vp, c_vp, ctypes.POINTER(c_i32)]),

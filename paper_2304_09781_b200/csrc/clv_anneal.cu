@@ -23,6 +23,9 @@
 // the accepted move to its own copy of the centre.
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include "clv_internal.h"
 
 namespace cg = cooperative_groups;
@@ -765,10 +768,27 @@ static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream
     auto kern = (a.n_ec == 1 && a.fast_div) ? anneal_kernel<MODE, MINB, UNR, PROF, true>
                                             : anneal_kernel<MODE, MINB, UNR, PROF, false>;
     const size_t smem = sizeof(AnnealSmem) + sizeof(RemEnt) * (size_t)(a.E * (a.E + 1) / 2);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
+    // The attribute calls and the cluster-size search (up to 15 occupancy queries) run
+    // once per (device, kernel, chains, shared bytes): a re-plan is ~1.5 ms, and these
+    // host calls sat between the caller's first event and the launch.
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void *, int, size_t>, int> chosen;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, reinterpret_cast<const void *>(kern), a.n_chains, smem);
+    int cached = 0;                              // auto cluster size (0: not searched yet)
+    bool attrs_set = false;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = chosen.find(key);
+        if (it != chosen.end()) { attrs_set = true; cached = it->second; }
+    }
+    if (!attrs_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(ANT, 1, 1);
     cfg.dynamicSmemBytes = smem;
@@ -779,7 +799,9 @@ static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cluster_size <= 0) {
+    if (cluster_size <= 0 && cached > 0) {
+        cluster_size = cached;
+    } else if (cluster_size <= 0) {
         // Largest cluster size that still keeps every chain resident (one wave).
         cluster_size = 1;
         for (int c = MAXCL; c >= 2; --c) {
@@ -792,6 +814,11 @@ static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream
             }
             cudaGetLastError();
         }
+        std::lock_guard<std::mutex> lk(mu);
+        chosen[key] = cluster_size;
+    } else if (!attrs_set) {
+        std::lock_guard<std::mutex> lk(mu);
+        chosen.emplace(key, 0);                  // attributes set; explicit sizes are not cached
     }
     cfg.gridDim = dim3((unsigned)(a.n_chains * cluster_size), 1, 1);
     attr[0].val.clusterDim.x = (unsigned)cluster_size;

@@ -173,7 +173,7 @@ void clv_destroy(clv_ctx *ctx) {
     cudaFree(ctx->ec_dev); cudaFree(ctx->small_dev);
     for (int f = 0; f < CLV_MAX_FAMILIES; ++f) cudaFree(ctx->pair_list_dev[f]);
     clv::sim_destroy(ctx->sim);
-    cudaFree(ctx->mvlog);
+    cudaFree(ctx->mvlog); cudaFree(ctx->replan_buf);
     delete ctx;
 }
 
@@ -600,6 +600,51 @@ int clv_select_chains(clv_ctx *ctx, const clv_chain_result *res, int n_chains, i
                       clv_record *rec_dev, void *stream) {
     if (!ctx) return CLV_ERR_CARBON_SCHED;
     CLV_CUDA(launch_select_chains(res, n_chains, chain_base, rec_dev, (cudaStream_t)stream), "select_chains");
+    return CLV_OK;
+}
+
+int clv_replan(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base, const uint16_t *start_w_host,
+               const clv_eval_params *params, int n_params, const clv_anneal_params *ap, uint64_t seed,
+               int cluster_size, clv_chain_result *results_host, uint16_t *best_w_host, uint16_t *final_w_host,
+               clv_record *record_host, void *stream) {
+    if (!ctx) return CLV_ERR_CARBON_SCHED;
+    int rc = need_family(ctx, family);
+    if (rc) return rc;
+    if (n_chains < 1) return fail(ctx, CLV_ERR_CARBON_SCHED, "a re-plan needs at least one chain");
+    if (!start_w_host || !results_host || !best_w_host || !final_w_host || !record_host)
+        return fail(ctx, CLV_ERR_CARBON_SCHED, "null host buffer");
+    const size_t E = (size_t)ctx->fam[family].E;
+    auto up16 = [](size_t b) { return (b + 15) & ~(size_t)15; };
+    const size_t b_in = up16(n_chains * E * 2), b_res = up16(n_chains * sizeof(clv_chain_result));
+    const size_t b_w = up16(n_chains * E * 2), b_rec = up16(sizeof(clv_record));
+    const size_t need = b_in + b_res + 2 * b_w + b_rec;
+    cudaStream_t st = (cudaStream_t)stream;
+    CLV_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (ctx->replan_cap < need) {
+        CLV_CUDA(cudaStreamSynchronize(st), "synchronize");
+        cudaFree(ctx->replan_buf);
+        ctx->replan_buf = nullptr; ctx->replan_cap = 0;
+        CLV_CUDA(cudaMalloc(&ctx->replan_buf, need), "alloc re-plan staging");
+        ctx->replan_cap = need;
+    }
+    unsigned char *b = ctx->replan_buf;
+    uint16_t *d_in = reinterpret_cast<uint16_t *>(b);
+    clv_chain_result *d_res = reinterpret_cast<clv_chain_result *>(b + b_in);
+    uint16_t *d_best = reinterpret_cast<uint16_t *>(b + b_in + b_res);
+    uint16_t *d_final = reinterpret_cast<uint16_t *>(b + b_in + b_res + b_w);
+    clv_record *d_rec = reinterpret_cast<clv_record *>(b + b_in + b_res + 2 * b_w);
+    CLV_CUDA(cudaMemcpyAsync(d_in, start_w_host, n_chains * E * 2, cudaMemcpyHostToDevice, st), "copy starts");
+    rc = clv_anneal(ctx, family, n, n_chains, chain_base, d_in, params, n_params, ap, seed, cluster_size, d_res,
+                    d_best, d_final, nullptr, stream);
+    if (rc) return rc;
+    rc = clv_select_chains(ctx, d_res, n_chains, chain_base, d_rec, stream);
+    if (rc) return rc;
+    CLV_CUDA(cudaMemcpyAsync(results_host, d_res, n_chains * sizeof(clv_chain_result), cudaMemcpyDeviceToHost, st),
+             "copy results");
+    CLV_CUDA(cudaMemcpyAsync(best_w_host, d_best, n_chains * E * 2, cudaMemcpyDeviceToHost, st), "copy best");
+    CLV_CUDA(cudaMemcpyAsync(final_w_host, d_final, n_chains * E * 2, cudaMemcpyDeviceToHost, st), "copy final");
+    CLV_CUDA(cudaMemcpyAsync(record_host, d_rec, sizeof(clv_record), cudaMemcpyDeviceToHost, st), "copy record");
+    CLV_CUDA(cudaStreamSynchronize(st), "synchronize");
     return CLV_OK;
 }
 

@@ -47,4 +47,6 @@ struct clv_ctx {
     clv::SimState *sim = nullptr;             // serving simulator (clv_sim.cu)
     int *mvlog = nullptr;                     // chain move logs (best-graph reconstruction)
     size_t mvlog_cap = 0;
+    unsigned char *replan_buf = nullptr;      // clv_replan device staging: starts | results | best | final | record
+    size_t replan_cap = 0;
 };

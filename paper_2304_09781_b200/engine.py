@@ -398,6 +398,48 @@ class CloverEngine:
                                         out.final_w.data_ptr(), _ptr(out.log), self._stream(stream)))
         return out
 
+    def replan(self, starts: np.ndarray, profile: ProfileTable, scenarios, ap: AnnealParams, seed: int,
+               chain_base: int = 0, cluster: int = 8, stream=None):
+        """One re-plan from host buffers in one native call (clv_replan): the starts are
+        staged in pinned memory, and the results, best / final graphs and the winner
+        record come back in pinned memory.  Returns host views (valid until the next
+        call): (results CHAIN_DTYPE[n], best_w uint16[n, E], final_w uint16[n, E], record)."""
+        fam = self.add_profile(profile)
+        starts = np.ascontiguousarray(starts, dtype=np.uint16)
+        n_chains, E = starts.shape
+        if E != profile.variant_count * 5:
+            raise CarbonSchedError("start graphs need %d edge weights" % (profile.variant_count * 5))
+        if isinstance(scenarios, Scenario):
+            scenarios = [scenarios]
+        # the ctypes argument structs of the last single-scenario call, reused while the
+        # caller passes the same (immutable) Scenario and AnnealParams objects
+        last = self.__dict__.get("_replan_args")
+        if len(scenarios) == 1 and last is not None and last[0] is scenarios[0] and last[1] is ap:
+            params, apc = last[2], last[3]
+        else:
+            params = (N.EvalParams * len(scenarios))(*[eval_params(x) for x in scenarios])
+            apc = N.AnnealParamsC(ap.t_init, ap.cooling_step, ap.t_floor, ap.stall_limit, ap.step_limit(),
+                                  1 if ap.proposal == "uniform" else 0, 1 if ap.evaluate == "proposal" else 0)
+            self._replan_args = (scenarios[0], ap, params, apc) if len(scenarios) == 1 else None
+        n = scenarios[0].n_gpus
+        self.ensure_feasibility(n)
+        nb_w = n_chains * E * 2
+        h_in = self.staging("rp_in", nb_w, pinned=True)
+        h_in.numpy()[:nb_w] = starts.view(np.uint8).reshape(-1)
+        r_b = n_chains * CHAIN_DTYPE.itemsize
+        h_out = self.staging("rp_out", r_b + 2 * nb_w + 32, pinned=True)
+        base = h_out.data_ptr()
+        self._check(self.lib.clv_replan(self.ctx, fam, n, n_chains, int(chain_base), h_in.data_ptr(), params,
+                                        len(scenarios), ctypes.byref(apc), int(seed) & ((1 << 64) - 1), int(cluster),
+                                        base, base + r_b, base + r_b + nb_w, base + r_b + 2 * nb_w,
+                                        self._stream(stream)))
+        raw = h_out.numpy()
+        res = raw[:r_b].view(CHAIN_DTYPE)
+        best_w = raw[r_b:r_b + nb_w].view(np.uint16).reshape(n_chains, E)
+        final_w = raw[r_b + nb_w:r_b + 2 * nb_w].view(np.uint16).reshape(n_chains, E)
+        record = raw[r_b + 2 * nb_w:r_b + 2 * nb_w + 32].view(RECORD_DTYPE)[0]
+        return res, best_w, final_w, record
+
     def select_chains(self, batch: AnnealBatch, record=None, stream=None):
         """Winner of a batch of chains as a 32-byte device record (SLA desc, h asc, chain asc)."""
         torch = self.torch

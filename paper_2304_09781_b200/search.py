@@ -126,6 +126,16 @@ def exchange_record(engine: CloverEngine, record, group=None):
     return engine.reduce_records(gathered)
 
 
+def _distributed(group, exchange: bool) -> bool:
+    """True when the winner record must be exchanged across ranks."""
+    if not exchange:
+        return False
+    import torch.distributed as dist
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        return False
+    return dist.get_world_size(group) > 1
+
+
 def anneal_chains(engine: CloverEngine, starts, profile: ProfileTable, scenarios, ap: AnnealParams,
                   seed: int, chain_base: int = 0, cluster: int = 8, log: bool = False, group=None,
                   exchange: bool = True) -> ChainsResult:
@@ -140,6 +150,14 @@ def anneal_chains(engine: CloverEngine, starts, profile: ProfileTable, scenarios
         starts = np.array([g.weights for g in starts], dtype=np.uint16)
     starts = np.ascontiguousarray(np.asarray(starts, dtype=np.uint16))
     n_chains, E = starts.shape
+    if not log and not _distributed(group, exchange):
+        # one native call: H2D, anneal, winner selection, D2H, synchronise (clv_replan)
+        res, best_w, final_w, record = engine.replan(starts, profile, scenarios, ap, seed, chain_base, cluster)
+        res, best_w, final_w = res.copy(), best_w.copy(), final_w.copy()
+        local = int(record["index"]) - chain_base
+        g = ConfigGraph(best_w[local].astype(np.int64), profile.variant_count, profile.name)
+        return ChainsResult(_result_from_chain(res[local], g), chain_base + local, res, best_w,
+                            final_w, int(res["evals"].sum()), record.copy(), None)
     # H2D: cached pinned staging buffer -> cached device buffer (one async copy)
     nb_in = starts.nbytes
     h_in = engine.staging("ac_in_host", nb_in, pinned=True)
