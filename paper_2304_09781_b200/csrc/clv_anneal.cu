@@ -411,7 +411,10 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
 }
 
 // Exact score of one neighbour folded into the thread's records.
-template <int MODE, bool EC1>
+// EC: 2 = one scenario for every chain, constants as kernel parameters, branch-free
+// division; 1 = per-chain scenarios (shared copy), branch-free division; 0 = per-chain
+// scenarios, IEEE division (a scenario outside fast_div_safe's ranges).
+template <int MODE, int EC>
 __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args, double t, double ac, double en,
                                      double id, double lmax, double mcnt, int idx, KRec &rS, KRec &rV, KRec &rP,
                                      uint64_t seed, uint64_t gchain, uint64_t k) {
@@ -423,8 +426,8 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args
     // one evaluation scenario for every chain: its constants are kernel parameters
     // (constant-bank operands); per-chain scenarios come from the CTA's shared copy
     Score sc;
-    if constexpr (EC1) sc = epilogue_t<true>(t, ac, en, id, lmax, mcnt, args.ec0);
-    else sc = epilogue_d(t, ac, en, id, lmax, mcnt, s.ec);
+    if constexpr (EC == 2) sc = epilogue_t<true>(t, ac, en, id, lmax, mcnt, args.ec0);
+    else sc = epilogue_t<EC == 1>(t, ac, en, id, lmax, mcnt, s.ec);
     const unsigned long long key = okey(sc.h);
     if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; } }
     else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; } }
@@ -446,7 +449,7 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args
 
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }   // finite operands
 
-template <int MODE, int MINB, int UNR, bool PROF = false, bool EC1 = false>
+template <int MODE, int MINB, int UNR, bool PROF = false, int EC = 0>
 __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
     long long prof_acc[PROF_SLOTS] = {};
     long long prof_last = 0;
@@ -559,7 +562,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (a != R.r1 && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]]) {
                     ++cnt;
                     const ARow &A = s.row[a];
-                    fold<MODE, EC1>(s, args, R.b0 + A.thr, R.b1 + A.acc, R.b2 + A.en,
+                    fold<MODE, EC>(s, args, R.b0 + A.thr, R.b1 + A.acc, R.b2 + A.en,
                                R.b3 + A.idle, dmax(s.lat_by_rank[R.top], s.lat_e[a]), mcnt, R.ibase + a,
                                rS, rV, rP, args.seed, gchain, (uint64_t)k);
                 }
@@ -597,7 +600,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                                 ++cnt;
                                 const int a1 = ent & 63, a2 = (ent >> 6) & 63;
                                 const ARow &A1 = s.row[a1], &A2 = s.row[a2];
-                                fold<MODE, EC1>(s, args, R.b0 + A1.thr + A2.thr, R.b1 + A1.acc + A2.acc,
+                                fold<MODE, EC>(s, args, R.b0 + A1.thr + A2.thr, R.b1 + A1.acc + A2.acc,
                                            R.b2 + A1.en + A2.en, R.b3 + A1.idle + A2.idle,
                                            dmax(s.lat_by_rank[R.top], dmax(s.lat_e[a1], s.lat_e[a2])), mcnt,
                                            R.ibase + (int)(ent >> 17), rS, rV, rP, args.seed,
@@ -763,10 +766,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
 
 template <int MODE, int MINB, int UNR, bool PROF = false>
 static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
-    // EC1: one scenario for every chain (constants as kernel parameters) whose ranges
-    // keep the branch-free divisions exact (fast_div_safe); else the general path
-    auto kern = (a.n_ec == 1 && a.fast_div) ? anneal_kernel<MODE, MINB, UNR, PROF, true>
-                                            : anneal_kernel<MODE, MINB, UNR, PROF, false>;
+    // branch-free divisions when every scenario keeps them exact (fast_div_safe)
+    auto kern = !a.fast_div ? anneal_kernel<MODE, MINB, UNR, PROF, 0>
+              : a.n_ec == 1 ? anneal_kernel<MODE, MINB, UNR, PROF, 2> : anneal_kernel<MODE, MINB, UNR, PROF, 1>;
     const size_t smem = sizeof(AnnealSmem) + sizeof(RemEnt) * (size_t)(a.E * (a.E + 1) / 2);
     // The attribute calls and the cluster-size search (up to 15 occupancy queries) run
     // once per (device, kernel, chains, shared bytes): a re-plan is ~1.5 ms, and these

@@ -561,7 +561,9 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
     CLV_CUDA(cudaMemcpyAsync(ctx->ec_dev, ecs.data(), sizeof(EvalConst) * n_params, cudaMemcpyHostToDevice, st), "copy eval consts");
     AnnealArgs a{};
     a.fam = ctx->fam_dev + family; a.F = feas_view(ctx); a.ec = ctx->ec_dev; a.n_ec = n_params; a.ec0 = ecs[0];
-    a.fast_div = fast_div_safe(ecs[0], ctx->fam[family].lat95, ctx->fam[family].E) ? 1 : 0;
+    a.fast_div = 1;
+    for (int i = 0; i < n_params; ++i)
+        if (!fast_div_safe(ecs[i], ctx->fam[family].lat95, ctx->fam[family].E)) a.fast_div = 0;
     a.t_init = ap->t_init; a.cooling = ap->cooling_step; a.t_floor = ap->t_floor;
     a.stall_limit = ap->stall_limit; a.max_steps = ap->max_steps; a.proposal = ap->proposal; a.evaluate = ap->evaluate;
     a.n = n; a.n_chains = n_chains; a.E = ctx->fam[family].E; a.chain_base = chain_base; a.seed = seed;

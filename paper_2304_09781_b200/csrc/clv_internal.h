@@ -131,7 +131,7 @@ struct AnnealArgs {
     const EvalConst *ec;
     int n_ec;
     EvalConst ec0;                  // = ec[0] when n_ec == 1 (kernel-parameter copy)
-    int fast_div;                   // ec0 and the family's lat95 satisfy fast_div_safe()
+    int fast_div;                   // every scenario and the family's lat95 satisfy fast_div_safe()
     double t_init, cooling, t_floor;
     int stall_limit, max_steps, proposal, evaluate;
     int n, n_chains, E;

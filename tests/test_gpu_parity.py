@@ -209,3 +209,21 @@ def test_run_trace_matches_oracle_controller(engine, feas64):
         assert row["sla_met"] == x["sla"]
         assert row["accuracy"] == x["accuracy"]
     assert rep.rows[-1]["cumulative_gco2"] == ref[-1]["cum"]
+
+
+@pytest.mark.parametrize("multi", [False, True])
+def test_anneal_exact_division_path(engine, feas64, multi):
+    """Scenarios outside fast_div_safe's ranges (here 1 - rho_sat < 1e-12) run the kernel
+    with IEEE divisions; single- and per-chain-scenario launches stay bit-exact."""
+    from dataclasses import replace
+    prof = synthetic_profile("efficientnet")
+    T = OracleTables.from_profile(prof)
+    n = 16
+    base = calibrate(prof, T, n, 380.0, 0.5)
+    scs = [replace(calibrate(prof, T, n, 380.0, lam), rho_sat=1.0 - 1e-13) for lam in (0.2, 0.5, 0.8)]
+    if not multi:
+        scs = scs[1:2]
+    assert base.rho_sat != scs[0].rho_sat
+    starts = random_fleet_graphs(T, n, 3, seed=77)
+    ap = AnnealParams(max_steps=16)
+    _chain_compare(engine, prof, T, starts, scs if multi else scs * 1, ap, 5, n, feas64, cluster=3)
