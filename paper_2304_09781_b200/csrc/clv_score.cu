@@ -625,7 +625,12 @@ struct __align__(32) SRow {
 
 constexpr int ZROW = CLV_MAX_EDGES;           // all-zero row: a configuration draw adds nothing
 
-template <bool FAST>
+// HIST: each variant draw only bumps the thread's 16-bit count of its edge ([edge][thread]
+// layout in shared memory: conflict-free), and the rows are applied once per edge after the
+// pod (S = sum_e count_e * row_e: the same exact integers, so the same fp64 sums); the
+// configuration's slice kinds and count come from one packed word, the pod's per-kind
+// variant counts from a register.  Counts stay below 2^16 while 7 * n_gpus < 65,536.
+template <bool FAST, bool HIST>
 __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ SweepArgs a) {
     __shared__ SRow row[CLV_MAX_PODS][CLV_MAX_EDGES + 1];
     __shared__ unsigned long long rbit[CLV_MAX_PODS][CLV_MAX_EDGES + 1];
@@ -634,6 +639,9 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
     __shared__ unsigned char flist[CLV_MAX_PODS][CLV_K][CLV_MAX_VARIANTS];
     __shared__ unsigned char nsl[CLV_MAX_CONFIGS];
     __shared__ unsigned char kinds[CLV_MAX_CONFIGS][8];
+    __shared__ __align__(16) unsigned cfgw[CLV_MAX_CONFIGS];   // kinds (3 bits each) | slice count << 24
+    __shared__ __align__(16) int pod_e[CLV_MAX_PODS];
+    __shared__ unsigned short hist[HIST ? (CLV_MAX_EDGES + 1) * SNT : 1];
     const Topology &P = *a.topo;
     for (int p = 0; p < a.n_pods; ++p) {
         const FamilyTables &T = a.fam[a.pods[p].family];
@@ -650,13 +658,22 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
             flist[p][t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS] = T.feas_list[t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS];
             if (t < CLV_K) nfeas[p][t] = T.nfeas[t];
         }
+        if (threadIdx.x == 0) pod_e[p] = T.E;
     }
     for (int r = threadIdx.x; r < P.K; r += SNT) {
         nsl[r] = (unsigned char)P.nslices[r];
-        for (int j = 0; j < 8; ++j) kinds[r][j] = P.kinds[r][j];
+        unsigned kw = 0;
+        for (int j = 0; j < 8; ++j) {
+            kinds[r][j] = P.kinds[r][j];
+            if (j < 7 && j < P.nslices[r]) kw |= (unsigned)P.kinds[r][j] << (3 * j);
+        }
+        cfgw[r] = kw | ((unsigned)P.nslices[r] << 24);
     }
+    if (HIST)
+        for (int q = threadIdx.x; q < (CLV_MAX_EDGES + 1) * SNT; q += SNT) hist[q] = 0;
     __syncthreads();
     const uint32_t K = (uint32_t)P.K;
+    unsigned short *hc = hist + (HIST ? threadIdx.x : 0);
     RecP r0 = recp_none(), r1 = recp_none();
     unsigned long long c_valid = 0, c_sla = 0;
     for (long long i = a.begin + (long long)blockIdx.x * SNT + threadIdx.x; i < a.end;
@@ -675,21 +692,52 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
             // all-zero row), so lanes stay converged until their last GPU.
             const int ng = a.pods[p].n_gpus;
             int g = 0, rem = 0, r = 0, slot = 0, inst = 0;
-            while (rem != 0 || g < ng) {
-                const uint32_t w = d.next();
-                const bool cfg = rem == 0;
-                const int k = kinds[r][slot & 7];
-                const int v = flist[p][k][(int)(((uint64_t)w * nfeas[p][k]) >> 32)];
-                const int e = cfg ? ZROW : v * 5 + k;
-                const SRow &q = row[p][e];
-                S0 += q.thr; S1 += q.acc; S2 += q.en; S3 += q.idle;
-                m |= rbit[p][e];
-                const int rn = (int)(((uint64_t)w * K) >> 32);
-                r = cfg ? rn : r;
-                rem = cfg ? (int)nsl[rn] : rem - 1;
-                slot = cfg ? 0 : slot + 1;
-                g += cfg ? 1 : 0;
-                inst += cfg ? 0 : 1;
+            if (HIST) {
+                unsigned nfw = 0;                        // per-kind feasible-variant counts, 4 bits each
+#pragma unroll
+                for (int k = 0; k < CLV_K; ++k) nfw |= (unsigned)nfeas[p][k] << (4 * k);
+                unsigned kw = 0;
+                while (rem != 0 || g < ng) {
+                    const uint32_t w = d.next();
+                    const bool cfg = rem == 0;
+                    const int k = kw & 7;
+                    const int v = flist[p][k][__umulhi(w, (nfw >> (4 * k)) & 15u)];
+                    const int e = cfg ? ZROW : v * 5 + k;
+                    hc[e * SNT] += 1;
+                    const unsigned cwn = cfgw[__umulhi(w, K)];
+                    kw = cfg ? (cwn & 0x1FFFFFu) : (kw >> 3);
+                    rem = cfg ? (int)(cwn >> 24) : rem - 1;
+                    g += cfg ? 1 : 0;
+                    inst += cfg ? 0 : 1;
+                }
+                const int E = pod_e[p];
+                for (int e = 0; e < E; ++e) {
+                    const unsigned c = hc[e * SNT];
+                    hc[e * SNT] = 0;
+                    const double cd = (double)c;
+                    const SRow &q = row[p][e];
+                    S0 = __fma_rn(cd, q.thr, S0); S1 = __fma_rn(cd, q.acc, S1);
+                    S2 = __fma_rn(cd, q.en, S2); S3 = __fma_rn(cd, q.idle, S3);
+                    m |= c ? rbit[p][e] : 0ULL;
+                }
+                hc[ZROW * SNT] = 0;
+            } else {
+                while (rem != 0 || g < ng) {
+                    const uint32_t w = d.next();
+                    const bool cfg = rem == 0;
+                    const int k = kinds[r][slot & 7];
+                    const int v = flist[p][k][(int)(((uint64_t)w * nfeas[p][k]) >> 32)];
+                    const int e = cfg ? ZROW : v * 5 + k;
+                    const SRow &q = row[p][e];
+                    S0 += q.thr; S1 += q.acc; S2 += q.en; S3 += q.idle;
+                    m |= rbit[p][e];
+                    const int rn = (int)(((uint64_t)w * K) >> 32);
+                    r = cfg ? rn : r;
+                    rem = cfg ? (int)nsl[rn] : rem - 1;
+                    slot = cfg ? 0 : slot + 1;
+                    g += cfg ? 1 : 0;
+                    inst += cfg ? 0 : 1;
+                }
             }
             Score sc = epilogue_t<FAST>(S0, S1, S2, S3, lat_by_rank[p][63 - __clzll((long long)m)], (double)inst,
                                   a.pods[p].ec);
@@ -712,8 +760,15 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
 }
 
 cudaError_t launch_sweep(const SweepArgs &a, int grid, cudaStream_t s) {
-    if (a.fast) sweep_kernel<true><<<grid, SNT, 0, s>>>(a);
-    else sweep_kernel<false><<<grid, SNT, 0, s>>>(a);
+    bool hist = true;                              // 16-bit edge counts cannot overflow
+    for (int p = 0; p < a.n_pods; ++p) hist = hist && 7LL * a.pods[p].n_gpus < 65536;
+    if (hist) {
+        if (a.fast) sweep_kernel<true, true><<<grid, SNT, 0, s>>>(a);
+        else sweep_kernel<false, true><<<grid, SNT, 0, s>>>(a);
+    } else {
+        if (a.fast) sweep_kernel<true, false><<<grid, SNT, 0, s>>>(a);
+        else sweep_kernel<false, false><<<grid, SNT, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 

@@ -190,6 +190,19 @@ def test_sweep_two_pods(engine):
     assert [(list(f.partitions), list(f.assignments)) for f in fleets] == [(p, a) for p, a in exp]
 
 
+def test_sweep_wide_pod_direct_sums(engine):
+    """A pod wider than the sweep's 16-bit edge counters allow (7 x 9,400 slices >= 2^16)
+    takes the per-draw row sums; same bits as the oracle."""
+    pr = synthetic_profile("resnet")
+    Tr = OracleTables.from_profile(pr)
+    n = 9400
+    sr = calibrate(pr, Tr, n, 300.0, 0.5)
+    f, h, sla = sweep_evaluate(7, 0, 3, [Pod(Tr, sr, n, 1.0)], DEFAULT_TOPOLOGY)
+    best, outs = engine.sweep([(pr, sr, n, 1.0)], 0, 3, 7, outputs=True)
+    assert bits_equal(outs["f"].cpu().numpy(), f)
+    assert bits_equal(outs["h"].cpu().numpy(), h)
+
+
 def test_run_trace_matches_oracle_controller(engine, feas64):
     from oracle.controller import run_trace_clover
     from paper_2304_09781_b200.controller import run_trace, ControllerParams
