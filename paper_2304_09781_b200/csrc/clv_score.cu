@@ -562,18 +562,19 @@ __global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ Ora
     const long long n = a.n;
     RecP r0 = recp_none(), r1 = recp_none();
     unsigned long long c_valid = 0, c_sla = 0;
+    int r = 0;                                 // a thread's indices ascend: resume the row search
     for (long long i = a.begin + (long long)blockIdx.x * SNT + threadIdx.x; i < a.end;
          i += (long long)gridDim.x * SNT) {
-        int r = 0;
         while (r + 1 < P.K && a.row_off[r + 1] <= i) ++r;
-        long long rem = i - a.row_off[r];
+        // within a row the index is < 8^7 (variants per slice ^ slices): 32-bit digits
+        unsigned rem = (unsigned)(i - a.row_off[r]);
         long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
         unsigned long long m = 0;
         const int ns = P.nslices[r];
         for (int j = 0; j < ns; ++j) {
-            const int pl = a.row_place[r][j];
+            const unsigned pl = (unsigned)a.row_place[r][j];
             const int dgt = (int)(rem / pl);
-            rem -= (long long)dgt * pl;
+            rem -= (unsigned)dgt * pl;
             const int k = P.kinds[r][j];
             const int e = flist[k][dgt] * 5 + k;
             S0 += row[e].thr; S1 += row[e].acc; S2 += row[e].en; S3 += row[e].idle;
