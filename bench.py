@@ -429,7 +429,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": 1000.0 * dev_time / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(args, world), "clocks": clk,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": ("search.anneal_chains -> clv_replan (one C-ABI call: pinned host starts H2D, anneal, "
+                             "winner selection, results D2H, synchronise)" if world == 1 else
+                             "search.anneal_chains -> clv_anneal + clv_select_chains + record all-gather + D2H")},
             "gpu_launches": launches_per_step * args.steps, "roofline": roof, "cpu_baseline": cpu,
             "replan_tts_ms": 1000.0 * dev_time / args.steps,
             "replan_tts_cpu_s": (None if cpu is None else (evals_all / args.steps) / cpu["value"]),
