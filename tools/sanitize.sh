@@ -13,6 +13,9 @@ for mode in ("best","uniform"):
     b=eng.anneal(st,prof,sc,AnnealParams(max_steps=3, proposal=mode),1,cluster=2)
 b=eng.anneal(st,prof,sc,AnnealParams(max_steps=3, proposal="uniform", evaluate="proposal"),1,cluster=3)
 best,_=eng.score_graphs(st,prof,sc)
+eng.replan(st,prof,sc,AnnealParams(max_steps=3),1,cluster=0)
+pr2=synthetic_profile("resnet"); s2=eng.calibrate(pr2,16,300.0,0.5)
+eng.sweep([(pr2,s2,16,0.5),(prof,eng.calibrate(prof,16,300.0,0.5),16,0.5)],0,3000,7)
 eng.oracle_search(prof, eng.calibrate(prof,1,400.0,0.5))
 import numpy as np
 from paper_2304_09781_b200.search import random_fleets
