@@ -321,7 +321,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             if (s.pfx[mid] <= q0) lo = mid; else hi = mid - 1;
         }
         int i = lo;
-#pragma unroll 1
+#pragma unroll
         for (int u = 0; u < PER; ++u) {
             const int q = q0 + u;
             if (u < per && q < npairs) {
@@ -359,8 +359,9 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
     const long long pt1 = PROF ? clock64() : 0;
     // (3) the removal entries (pairs: every thread; singles: the last warp)
     int lpos = s.warp_len[wid] + il - lsum;
-#pragma unroll 1
-    for (int u = 0; u < cnt; ++u) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {              // fixed trip count: the entries' loads overlap
+        if (u >= cnt) break;
         const int pkv = s.pk[q0 + u];
         const int p = pkv & 1023, x = (pkv >> 10) & 63, y = pkv >> 16;
         RemEnt &r = rp[q0 + u];
