@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define CLV_ABI_VERSION 1
+#define CLV_ABI_VERSION 2
 #define CLV_MAX_VARIANTS 8
 #define CLV_MAX_EDGES 40
 #define CLV_MAX_CONFIGS 32
@@ -165,10 +165,15 @@ uint64_t clv_derive_seed(const uint64_t *parts, int n_parts);
 
 int clv_set_topology(clv_ctx *ctx, int n_configs, const int32_t *config_ids,
                      const int32_t *counts5, const double *memory_gb5);
+/* Scoring rows of one profile family, edge e = (v-1)*5 + slice index:
+ * fixed-point thr/acc/en rows, per-slice idle row, lat95 = p95 service time (ms, the value
+ * a p95 estimate reports) and svc = mean service time (ms, the request shares of the
+ * instance-pull p95 walk); both > 0, and lat95 must order the edges like svc
+ * (one distribution family per catalog). */
 int clv_set_profile(clv_ctx *ctx, int family, int n_variants,
                     const int64_t *thr_q, const int64_t *acc_q, const int64_t *en_q,
-                    const int64_t *idle_q5, const double *lat95, const uint8_t *mem_ok,
-                    int kt, int ke, int ki);
+                    const int64_t *idle_q5, const double *lat95, const double *svc_ms,
+                    const uint8_t *mem_ok, int kt, int ke, int ki);
 int clv_build_feasibility(clv_ctx *ctx, int n_max, void *stream);
 int64_t clv_feasibility_bytes(const clv_ctx *ctx);
 

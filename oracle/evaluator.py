@@ -1,7 +1,13 @@
 """ORACLE -- TEST INFRASTRUCTURE ONLY.  The table-surrogate evaluator.
 
 Restates DESIGN.md "Scoring surrogate" (the replacement for SPEC:334-372's DES,
-SURVEY 7.2 D1) and Eqs. 1, 2, 3, 6 in numpy.  Eq. 1 / Eq. 2 use
+SURVEY 7.2 D1) and Eqs. 1, 2, 3, 6 in numpy.  The p95 term is the
+nearest-rank p95 over requests of the fleet's service-time mixture:
+request shares follow the instance-pull dispatch of SPEC:335 at utilisation
+rho < 1 (every instance waits W0 = (1000 m / R)(1 - rho) ms in the idle queue
+between services, so instance j serves 1000 / (s_j + W0) requests/s; W0 -> 0
+gives SPEC:390's throughput shares under saturation), walked from the slowest
+edge down until the tail holds more than 5 % of the arrival rate R.  Eq. 1 / Eq. 2 use
 the algebraically identical forms (A - A_base) * (100 / A_base) and
 100 - E * (ci / (10 C_base)); tests pin them to the SPEC-literal quotients.
 Aggregates are recomputed from scratch per candidate (W @ rows, int64), so this
@@ -34,7 +40,42 @@ def constants(tables: OracleTables, scenario):
     R = float(scenario.arrival_rps)
     return dict(R_q=math.ldexp(R, tables.kt), inv_3600R=1.0 / (3600.0 * R),
                 en_scale=math.ldexp(1.0, tables.kt - tables.ke),
-                idle_scale=math.ldexp(1.0, -tables.ki))
+                idle_scale=math.ldexp(1.0, -tables.ki),
+                kW=1000.0 / R, c20=20000.0 / R)
+
+
+def rank_order(tables: OracleTables) -> list:
+    """Edges by ascending p95 service latency, ties by edge index (the device's rank)."""
+    return sorted(range(tables.E), key=lambda e: (float(tables.lat95[e]), e))
+
+
+def p95_walk(W: np.ndarray, tables: OracleTables, W0: np.ndarray, c20: float) -> np.ndarray:
+    """Service p95 of each fleet (rows of W) given its idle-queue time W0 (ms).
+
+    Present edges are visited from the highest latency rank down; the tail's request
+    rate sum_j 1000 w_j / (s_j + W0) is kept as the fraction P / Q (no division):
+    d = s + W0, P <- P d + w Q, Q <- Q d; the walk stops at the first edge where
+    P * (20000 / R) > Q (the tail now holds > 5 % of R), else at the lowest present
+    edge.  The p95 is that edge's lat95."""
+    W = np.asarray(W, dtype=np.int64).reshape(-1, tables.E)
+    n = len(W)
+    P = np.zeros(n)
+    Q = np.ones(n)
+    done = np.zeros(n, dtype=bool)
+    lq = np.zeros(n)
+    with np.errstate(over="ignore", invalid="ignore"):
+        for e in reversed(rank_order(tables)):
+            act = ~done & (W[:, e] > 0)
+            if not act.any():
+                continue
+            d = float(tables.mean_ms[e]) + W0
+            Pn = P * d + W[:, e].astype(np.float64) * Q
+            Qn = Q * d
+            P = np.where(act, Pn, P)
+            Q = np.where(act, Qn, Q)
+            lq = np.where(act, float(tables.lat95[e]), lq)
+            done = done | (act & (P * c20 > Q))
+    return lq
 
 
 def aggregates(W: np.ndarray, tables: OracleTables):
@@ -44,12 +85,11 @@ def aggregates(W: np.ndarray, tables: OracleTables):
     s_en = W @ tables.en_q
     cnt = W.reshape(len(W), tables.V, 5).sum(axis=1)
     s_idle = cnt @ tables.idle_q
-    lmax = np.where(W > 0, tables.lat95[None, :], -np.inf).max(axis=1)
     m = W.sum(axis=1)
-    return s_thr, s_acc, s_en, s_idle, lmax, m
+    return s_thr, s_acc, s_en, s_idle, W, m
 
 
-def epilogue(s_thr, s_acc, s_en, s_idle, lmax, m, tables, scenario) -> Evaluated:
+def epilogue(s_thr, s_acc, s_en, s_idle, W, m, tables, scenario) -> Evaluated:
     c = constants(tables, scenario)
     obj = scenario.obj
     a_base, c_base, slo = obj.base_accuracy, obj.base_carbon_g, obj.latency_slo_ms
@@ -64,14 +104,17 @@ def epilogue(s_thr, s_acc, s_en, s_idle, lmax, m, tables, scenario) -> Evaluated
         rho_c = np.minimum(rho, 1.0)
         p_idle = s_idle.astype(np.float64) * c["idle_scale"]
         E = e_act + ((1.0 - rho_c) * p_idle) * c["inv_3600R"]
+        md = np.asarray(m, dtype=np.float64)
+        W0 = (md * c["kW"]) * (1.0 - rho_c)           # idle-queue time between services (ms)
+        lq = p95_walk(W, tables, W0, c["c20"])
         rho_q = np.minimum(rho, scenario.rho_sat)
-        # many-server p95: L = Lmax * (1 + rho^8 / (m (1 - rho)))
+        # queueing factor of m servers: L = lq * (1 + rho^8 / (m (1 - rho)))
         q1 = 1.0 - rho_q
         r2 = rho_q * rho_q
         r4 = r2 * r2
         r8 = r4 * r4
-        wq = r8 / (np.asarray(m, dtype=np.float64) * q1)
-        L = lmax * (1.0 + wq)
+        wq = r8 / (md * q1)
+        L = lq * (1.0 + wq)
         dA = (A - a_base) * kA
         dC = 100.0 - E * kC
         f = lam * dC + (1.0 - lam) * dA

@@ -84,7 +84,7 @@ SIGNATURES = {
     "clv_last_error": (ctypes.c_char_p, [c_vp]),
     "clv_derive_seed": (c_u64, [ctypes.POINTER(c_u64), c_i32]),
     "clv_set_topology": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp]),
-    "clv_set_profile": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32]),
+    "clv_set_profile": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32]),
     "clv_build_feasibility": (c_i32, [c_vp, c_i32, c_vp]),
     "clv_feasibility_bytes": (c_i64, [c_vp]),
     "clv_feasible": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_vp, c_vp]),
@@ -126,7 +126,7 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.clv_abi_version() != 1:
+    if lib.clv_abi_version() != 2:
         raise E.DeviceError("ABI version mismatch")
     _lib = lib
     return lib

@@ -11,11 +11,12 @@
 // oracle's int64 W @ rows bit for bit), per-edge p95 latencies, the family's
 // static double-move lists (offsets/lengths), the chain centre, and per step the
 // removal table: one entry per present edge (singles) and per available removal
-// pair (doubles) with the exact removal deltas, the highest-latency edge that
-// stays present after the removal, and the entry's share of the move space.
+// pair (doubles) with the exact removal deltas, the latency-rank presence mask that
+// remains after the removal, and the entry's share of the move space.
 // A neighbour is then scored as
-//   S' = S + removal.d + row[a1] (+ row[a2]),  Lmax' = max(lat[removal.top], lat[a1], lat[a2])
-// followed by the fp64 epilogue (clv_common.cuh).  Every CTA of the cluster
+//   S' = S + removal.d + row[a1] (+ row[a2]),  pm' = removal.pm | bit(a1) | bit(a2)
+// followed by the fp64 epilogue (clv_common.cuh), whose p95 walk reads the centre's
+// per-rank weights corrected by the (<= 4) changed edges.  Every CTA of the cluster
 // builds identical tables (ordered compaction) and scores a contiguous share of
 // the flattened move space; each CTA's two SLA-class records and hash record are
 // broadcast to every CTA of the cluster over DSMEM, and after ONE cluster barrier
@@ -45,15 +46,16 @@ struct __align__(16) ARow {
     double thr, acc, en, idle;
 };
 
-struct __align__(8) RemEnt {            // one removal multiset R (single edge or pair), 56 B
+struct __align__(8) RemEnt {            // one removal multiset R (single edge or pair), 64 B
     double b0, b1, b2, b3;                 // centre aggregates minus the rows of R (exact integers)
+    unsigned long long pm;                 // latency-rank presence mask after the removal
     int pre;                               // doubles: exclusive prefix of move-list lengths
     int end;                               // doubles: pre + move-list length
     int offm;                              // doubles: first static move-list entry minus pre
     int ibase;                             // canonical index base: E*E + P(r1,r2)*NP (doubles), r*E (singles)
     unsigned short code;                   // slice code of R: sr1*125 + sr2*25 (doubles), sr*5 (singles)
     unsigned char r1, r2;                  // removed edges (r2 = 0xFF for singles)
-    unsigned char top;                     // latency rank of the top edge still present, NO_TOP if none
+    unsigned char k1, k2;                  // their latency ranks (k2 = 0xFF for singles)
 };
 
 struct KRec {                              // (key, idx) record; payload hv (uniform proposals)
@@ -97,9 +99,12 @@ __device__ __forceinline__ KRec krec_min_redux(KRec r) {
 
 struct __align__(16) AnnealSmem {
     ARow row[CLV_MAX_EDGES];
-    double lat_e[CLV_MAX_EDGES];           // p95 latency per edge
     double lat_by_rank[CLV_MAX_EDGES + 1]; // ascending; [NO_TOP] = 0
+    double svc_by_rank[CLV_MAX_EDGES];     // mean service time at each latency rank (p95 walk)
+    double wr[CLV_MAX_EDGES];              // centre weight at each latency rank
     unsigned long long rbit[CLV_MAX_EDGES];// 1 << latency rank
+    unsigned char rk[CLV_MAX_EDGES];       // latency rank of the edge
+    unsigned char er[CLV_MAX_EDGES];       // edge at each latency rank
     EvalConst ec;
     unsigned long long mem_ok;
     unsigned magicE, magicNP;              // ceil(2^32 / E), ceil(2^32 / NP) (exact small divisions)
@@ -132,9 +137,34 @@ struct __align__(16) AnnealSmem {
     int bw[CLV_MAX_EDGES];                 // best graph (rank 0)
 };
 
-__device__ __forceinline__ double lmax_of(const AnnealSmem &s, unsigned long long m) {
-    return m ? s.lat_by_rank[63 - __clzll((long long)m)] : 0.0;
-}
+// Service p95 of the centre corrected by removals (ranks k1, k2) and additions (ranks
+// j1, j2); 0xFF = absent.  pm: the candidate's presence mask by latency rank.
+struct CandWalk {
+    const AnnealSmem *s;
+    unsigned long long pm;
+    double c20;
+    int k1, k2, j1, j2;
+    __device__ __forceinline__ double operator()(double W0) const {
+        const AnnealSmem &S = *s;
+        const int a = k1, b = k2, c = j1, d = j2;
+        return p95_walk(pm, W0, c20, S.svc_by_rank, S.lat_by_rank, [&](int r) {
+            return S.wr[r] + (double)((r == c) + (r == d) - (r == a) - (r == b));
+        });
+    }
+};
+// Service p95 of an explicit weight vector (rank 0 / thread 0 paths).
+struct GraphWalk {
+    const AnnealSmem *s;
+    const int *w;                          // weights by edge
+    const unsigned char *edge_of_rank;
+    unsigned long long pm;
+    double c20;
+    __device__ __forceinline__ double operator()(double W0) const {
+        const int *ww = w;
+        const unsigned char *eo = edge_of_rank;
+        return p95_walk(pm, W0, c20, s->svc_by_rank, s->lat_by_rank, [&](int r) { return (double)ww[eo[r]]; });
+    }
+};
 
 // canonical index -> move (r1, r2, a1, a2; 0xFF = absent); indices are < 2^31
 __device__ inline void decode_move(const AnnealSmem &s, int E, long long idx64, int &r1, int &r2, int &a1, int &a2) {
@@ -168,7 +198,9 @@ __device__ inline Score score_move(const AnnealSmem &s, int r1, int r2, int a1, 
         t += s.row[f[k]].thr; ac += s.row[f[k]].acc; en += s.row[f[k]].en; id += s.row[f[k]].idle;
         m |= s.rbit[f[k]];
     }
-    return epilogue_d(t, ac, en, id, lmax_of(s, m), s.mcount, s.ec);
+    CandWalk cw{&s, m, s.ec.c20, r1 == 0xFF ? 0xFF : s.rk[r1], r2 == 0xFF ? 0xFF : s.rk[r2],
+                a1 == 0xFF ? 0xFF : s.rk[a1], a2 == 0xFF ? 0xFF : s.rk[a2]};
+    return epilogue_d(t, ac, en, id, s.mcount, s.ec, cw);
 }
 
 // Apply a move to a bare weight vector (best-graph reconstruction).
@@ -206,6 +238,9 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
     s.w[r1] = nr1;
     s.w[a1] = na1;
     if (two) { s.w[r2] = nr2; s.w[a2] = (a2 == a1) ? na1 : wa2 + 1; }
+    s.wr[s.rk[r1]] = (double)s.w[r1];
+    s.wr[s.rk[a1]] = (double)s.w[a1];
+    if (two) { s.wr[s.rk[r2]] = (double)s.w[r2]; s.wr[s.rk[a2]] = (double)s.w[a2]; }
     const int kr1 = r1 % CLV_K, ka1 = a1 % CLV_K, kr2 = two ? r2 % CLV_K : -1, ka2 = two ? a2 % CLV_K : -1;
 #pragma unroll
     for (int k = 0; k < CLV_K; ++k)
@@ -213,10 +248,6 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
     if (nr1 == 0) m &= ~br1;
     if (nr2 == 0) m &= ~br2;
     s.pmask = m | ba1 | ba2;
-}
-
-__device__ __forceinline__ unsigned char top_rank(unsigned long long m) {
-    return m ? (unsigned char)(63 - __clzll((long long)m)) : (unsigned char)NO_TOP;
 }
 
 // Per-step tables: deterministic ordered compaction of the removal pairs (every
@@ -375,7 +406,8 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             if (s.w[x] == 1) m &= ~s.rbit[x];
             if (s.w[y] == 1) m &= ~s.rbit[y];
         }
-        r.top = top_rank(m);
+        r.pm = m;
+        r.k1 = s.rk[x]; r.k2 = s.rk[y];
         r.ibase = E * E + p * NP;
         r.pre = lpos;
         r.offm = s.pair_off[p] - lpos;
@@ -390,7 +422,8 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             RemEnt &r = s.se[i];
             r.b0 = s.S[0] + -s.row[e].thr; r.b1 = s.S[1] + -s.row[e].acc;
             r.b2 = s.S[2] + -s.row[e].en; r.b3 = s.S[3] + -s.row[e].idle;
-            r.top = top_rank((s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask);
+            r.pm = (s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask;
+            r.k1 = s.rk[e]; r.k2 = 0xFF;
             r.ibase = e * E;
             r.code = (unsigned short)(s.sl[e] * 5);
             r.r1 = (unsigned char)e; r.r2 = 0xFF; r.offm = 0; r.end = 0; r.pre = 0;
@@ -417,8 +450,8 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
 // scenarios, IEEE division (a scenario outside fast_div_safe's ranges).
 template <int MODE, int EC>
 __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args, double t, double ac, double en,
-                                     double id, double lmax, double mcnt, int idx, KRec &rS, KRec &rV, KRec &rP,
-                                     uint64_t seed, uint64_t gchain, uint64_t k) {
+                                     double id, const CandWalk &cw, double mcnt, int idx, KRec &rS, KRec &rV,
+                                     KRec &rP, uint64_t seed, uint64_t gchain, uint64_t k) {
     if (MODE == MODE_UNIFORM_PROPOSAL) {
         const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
         if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; }
@@ -427,8 +460,8 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args
     // one evaluation scenario for every chain: its constants are kernel parameters
     // (constant-bank operands); per-chain scenarios come from the CTA's shared copy
     Score sc;
-    if constexpr (EC == 2) sc = epilogue_t<true>(t, ac, en, id, lmax, mcnt, args.ec0);
-    else sc = epilogue_t<EC == 1>(t, ac, en, id, lmax, mcnt, s.ec);
+    if constexpr (EC == 2) sc = epilogue_t<true>(t, ac, en, id, mcnt, args.ec0, cw);
+    else sc = epilogue_t<EC == 1>(t, ac, en, id, mcnt, s.ec, cw);
     const unsigned long long key = okey(sc.h);
     if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; } }
     else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; } }
@@ -447,8 +480,6 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args
         if ((ph) > 0) prof_acc[(ph) - 1] += _now - prof_last;                          \
         prof_last = _now;                                                              \
     }
-
-__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }   // finite operands
 
 template <int MODE, int MINB, int UNR, bool PROF = false, int EC = 0>
 __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
@@ -474,9 +505,11 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         s.row[e].acc = (double)T.acc_q[e];
         s.row[e].en = (double)T.en_q[e];
         s.row[e].idle = (double)T.idle_q[e % 5];
-        s.lat_e[e] = T.lat95[e];
         s.lat_by_rank[e] = T.lat_by_rank[e];
+        s.svc_by_rank[e] = T.svc_by_rank[e];
         s.rbit[e] = 1ULL << T.rank[e];
+        s.rk[e] = T.rank[e];
+        s.er[e] = T.edge_by_rank[e];
         s.sl[e] = (unsigned char)(e % 5);
     }
     for (int x = tid; x < E; x += ANT)
@@ -505,7 +538,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         s.S[0] = S0; s.S[1] = S1; s.S[2] = S2; s.S[3] = S3;
         s.pmask = m;
         int cnt = 0;
-        for (int e = 0; e < E; ++e) cnt += s.w[e];
+        for (int e = 0; e < E; ++e) { cnt += s.w[e]; s.wr[s.rk[e]] = (double)s.w[e]; }
         s.mcount = (double)cnt;
     }
     __syncthreads();
@@ -526,7 +559,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         }
         if (tot < 1 || !feasible(args.F, n, s.svec[0], s.svec[1], s.svec[2], s.svec[3], s.svec[4])) invalid = 1;
         edge_evals = __popcll(s.pmask);
-        const Score sc = epilogue_d(s.S[0], s.S[1], s.S[2], s.S[3], lmax_of(s, s.pmask), s.mcount, s.ec);
+        const Score sc = epilogue_d(s.S[0], s.S[1], s.S[2], s.S[3], s.mcount, s.ec,
+                                    GraphWalk{&s, s.w, s.er, s.pmask, s.ec.c20});
         hc = sc.h;
         bk1 = sc.sla ? 0u : 1u; bk2 = okey(sc.h);
         for (int e = 0; e < E; ++e) s.bw[e] = s.w[e];
@@ -539,6 +573,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     const int G = CL * ANT;
     const int gt = crank * ANT + tid;
     const unsigned long long mem_ok = s.mem_ok;
+    const double c20 = EC == 2 ? args.ec0.c20 : s.ec.c20;
 
     for (int k = 0; !done; ++k) {
         PROF_MARK(0);
@@ -563,8 +598,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (a != R.r1 && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]]) {
                     ++cnt;
                     const ARow &A = s.row[a];
+                    const CandWalk cw{&s, R.pm | s.rbit[a], c20, R.k1, 0xFF, s.rk[a], 0xFF};
                     fold<MODE, EC>(s, args, R.b0 + A.thr, R.b1 + A.acc, R.b2 + A.en,
-                               R.b3 + A.idle, dmax(s.lat_by_rank[R.top], s.lat_e[a]), mcnt, R.ibase + a,
+                               R.b3 + A.idle, cw, mcnt, R.ibase + a,
                                rS, rV, rP, args.seed, gchain, (uint64_t)k);
                 }
                 i += dI; a += dA;
@@ -601,9 +637,10 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                                 ++cnt;
                                 const int a1 = ent & 63, a2 = (ent >> 6) & 63;
                                 const ARow &A1 = s.row[a1], &A2 = s.row[a2];
+                                const CandWalk cw{&s, R.pm | s.rbit[a1] | s.rbit[a2], c20, R.k1, R.k2,
+                                                  s.rk[a1], s.rk[a2]};
                                 fold<MODE, EC>(s, args, R.b0 + A1.thr + A2.thr, R.b1 + A1.acc + A2.acc,
-                                           R.b2 + A1.en + A2.en, R.b3 + A1.idle + A2.idle,
-                                           dmax(s.lat_by_rank[R.top], dmax(s.lat_e[a1], s.lat_e[a2])), mcnt,
+                                           R.b2 + A1.en + A2.en, R.b3 + A1.idle + A2.idle, cw, mcnt,
                                            R.ibase + (int)(ent >> 17), rS, rV, rP, args.seed,
                                            gchain, (uint64_t)k);
                             }
@@ -756,7 +793,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             S0 += x * s.row[e].thr; S1 += x * s.row[e].acc; S2 += x * s.row[e].en; S3 += x * s.row[e].idle;
             if (x > 0) m |= s.rbit[e];
         }
-        const Score sb = epilogue_d(S0, S1, S2, S3, lmax_of(s, m), s.mcount, s.ec);   // moves keep m
+        const Score sb = epilogue_d(S0, S1, S2, S3, s.mcount, s.ec, GraphWalk{&s, s.bw, s.er, m, s.ec.c20});   // moves keep m
         r.f = sb.f; r.h = sb.h; r.p95_ms = sb.L; r.accuracy = sb.A; r.energy_wh = sb.E;
         r.sla_met = sb.sla;
         r.status = status; r.steps = steps; r.best_step = best_step;

@@ -48,6 +48,8 @@ int make_ec(clv_ctx *ctx, const clv_eval_params *p, const FamilyTables &T, EvalC
     double R = p->arrival_rps;
     ec.R_q = std::ldexp(R, T.kt);
     ec.inv_3600R = 1.0 / (3600.0 * R);
+    ec.kW = 1000.0 / R;
+    ec.c20 = 20000.0 / R;
     ec.en_scale = std::ldexp(1.0, T.kt - T.ke);
     ec.idle_scale = std::ldexp(1.0, -T.ki);
     ec.rho_sat = p->rho_sat;
@@ -234,7 +236,7 @@ int clv_set_topology(clv_ctx *ctx, int K, const int32_t *ids, const int32_t *cou
 
 int clv_set_profile(clv_ctx *ctx, int family, int V, const int64_t *thr_q, const int64_t *acc_q,
                     const int64_t *en_q, const int64_t *idle_q5, const double *lat95,
-                    const uint8_t *mem_ok, int kt, int ke, int ki) {
+                    const double *svc_ms, const uint8_t *mem_ok, int kt, int ke, int ki) {
     if (!ctx) return CLV_ERR_CARBON_SCHED;
     if (family < 0 || family >= CLV_MAX_FAMILIES) return fail(ctx, CLV_ERR_PROFILE, "family out of range");
     if (V < 1 || V > CLV_MAX_VARIANTS) return fail(ctx, CLV_ERR_PROFILE, "1..8 variants supported on the device");
@@ -245,7 +247,9 @@ int clv_set_profile(clv_ctx *ctx, int family, int V, const int64_t *thr_q, const
         if (thr_q[e] <= 0 || thr_q[e] >= LIM || acc_q[e] < 0 || acc_q[e] >= LIM || en_q[e] < 0 || en_q[e] >= LIM)
             return fail(ctx, CLV_ERR_PROFILE, "fixed-point rows must be in [0, 2^31) (throughput > 0)");
         if (!(lat95[e] > 0) || !is_finite(lat95[e])) return fail(ctx, CLV_ERR_PROFILE, "p95 service time must be positive");
+        if (!(svc_ms[e] > 0) || !is_finite(svc_ms[e])) return fail(ctx, CLV_ERR_PROFILE, "mean service time must be positive");
         T.thr_q[e] = thr_q[e]; T.acc_q[e] = acc_q[e]; T.en_q[e] = en_q[e]; T.lat95[e] = lat95[e];
+        T.svc[e] = svc_ms[e];
         if (mem_ok[e]) T.mem_ok |= 1ULL << e;
     }
     for (int k = 0; k < CLV_K; ++k) {
@@ -257,7 +261,10 @@ int clv_set_profile(clv_ctx *ctx, int family, int V, const int64_t *thr_q, const
     std::sort(ord.begin(), ord.end(), [&](int x, int y) {
         return T.lat95[x] != T.lat95[y] ? T.lat95[x] < T.lat95[y] : x < y;
     });
-    for (int r = 0; r < T.E; ++r) { T.rank[ord[r]] = (unsigned char)r; T.lat_by_rank[r] = T.lat95[ord[r]]; }
+    for (int r = 0; r < T.E; ++r) {
+        T.rank[ord[r]] = (unsigned char)r; T.lat_by_rank[r] = T.lat95[ord[r]];
+        T.svc_by_rank[r] = T.svc[ord[r]]; T.edge_by_rank[r] = (unsigned char)ord[r];
+    }
     int nbmax = 0;
     for (int e = 0; e < T.E; ++e) {
         int c = 0;

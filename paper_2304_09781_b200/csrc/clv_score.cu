@@ -5,8 +5,8 @@
 //  score_graphs : uint16 graph rows (E = 5V per row) streamed from HBM through a
 //                 shared-memory tile, exact int64 aggregates, fp64 epilogue,
 //                 fleet-feasibility lookup, grid argmax.       HBM/issue bound
-//  score_x      : FleetConfig (x^p, x^v) CSR rows decoded by one warp each
-//                 (shuffle prefix-sum of slices per GPU, mig.py:286-296)
+//  score_x      : FleetConfig (x^p, x^v) CSR rows decoded by one thread each over a
+//                 shared-memory tile (mig.py:286-296)
 //  oracle       : index -> (config id, mixed-radix variant digits)
 //  sweep        : index -> counter-RNG draws -> per-pod graphs
 #include <algorithm>
@@ -20,17 +20,45 @@ struct __align__(16) ERow {
     long long thr, acc, en, idle;
 };
 
-__device__ inline void stage_rows(ERow *row, double *lat_by_rank, unsigned char *rank,
-                                  const FamilyTables &T) {
+struct RankTabs {                             // per-family latency-rank tables (shared memory)
+    double lat[CLV_MAX_EDGES];                 // lat95 by rank
+    double svc[CLV_MAX_EDGES];                 // mean service time by rank
+    unsigned char edge[CLV_MAX_EDGES];         // edge at each rank
+    unsigned char rank[CLV_MAX_EDGES];         // rank of each edge
+};
+
+__device__ inline void stage_ranks(RankTabs &rt, const FamilyTables &T) {
+    for (int e = threadIdx.x; e < T.E; e += blockDim.x) {
+        rt.lat[e] = T.lat_by_rank[e];
+        rt.svc[e] = T.svc_by_rank[e];
+        rt.edge[e] = T.edge_by_rank[e];
+        rt.rank[e] = T.rank[e];
+    }
+}
+
+__device__ inline void stage_rows(ERow *row, RankTabs &rt, const FamilyTables &T) {
     for (int e = threadIdx.x; e < T.E; e += blockDim.x) {
         row[e].thr = T.thr_q[e];
         row[e].acc = T.acc_q[e];
         row[e].en = T.en_q[e];
         row[e].idle = T.idle_q[e % 5];
-        lat_by_rank[e] = T.lat_by_rank[e];
-        rank[e] = T.rank[e];
     }
+    stage_ranks(rt, T);
 }
+
+// p95 walker over a weight vector indexed by edge (any integer element type)
+template <class W>
+struct EdgeWalk {
+    const RankTabs *rt;
+    const W *w;
+    unsigned long long pm;                     // presence by latency rank
+    double c20;
+    __device__ __forceinline__ double operator()(double W0) const {
+        const RankTabs &t = *rt;
+        const W *ww = w;
+        return p95_walk(pm, W0, c20, t.svc, t.lat, [&](int r) { return (double)ww[t.edge[r]]; });
+    }
+};
 
 __device__ inline void consider(RecP &r0, RecP &r1, const Score &sc, long long idx, int mode) {
     RecP c;
@@ -56,11 +84,10 @@ __device__ inline void consider(RecP &r0, RecP &r1, const Score &sc, long long i
 template <bool VEC>
 __global__ void __launch_bounds__(SNT) score_graphs_kernel(const __grid_constant__ ScoreArgs a) {
     __shared__ ERow row[CLV_MAX_EDGES];
-    __shared__ double lat_by_rank[CLV_MAX_EDGES];
-    __shared__ unsigned char rank[CLV_MAX_EDGES];
+    __shared__ RankTabs rt;
     __shared__ __align__(16) uint16_t tile[SNT * CLV_MAX_EDGES];
     const FamilyTables &T = *a.fam;
-    stage_rows(row, lat_by_rank, rank, T);
+    stage_rows(row, rt, T);
     const int E = T.E;
     const unsigned long long mem_ok = T.mem_ok;
     const int n = a.ec.n;
@@ -91,15 +118,16 @@ __global__ void __launch_bounds__(SNT) score_graphs_kernel(const __grid_constant
                 if (x) {
                     S0 += x * row[e].thr; S1 += x * row[e].acc; S2 += x * row[e].en; S3 += x * row[e].idle;
                     sv[e % 5] += (int)x;
-                    m |= 1ULL << rank[e];
+                    m |= 1ULL << rt.rank[e];
                     memfail |= !((mem_ok >> e) & 1ULL);
                 }
             }
             const long long i = base + threadIdx.x;
             const bool feas = !memfail && m != 0 && feasible(a.F, n, sv[0], sv[1], sv[2], sv[3], sv[4]);
             if (feas) {
-                Score sc = epilogue(S0, S1, S2, S3, lat_by_rank[63 - __clzll((long long)m)],
-                                    (double)(sv[0] + sv[1] + sv[2] + sv[3] + sv[4]), a.ec);
+                Score sc = epilogue_d((double)S0, (double)S1, (double)S2, (double)S3,
+                                      (double)(sv[0] + sv[1] + sv[2] + sv[3] + sv[4]), a.ec,
+                                      EdgeWalk<uint16_t>{&rt, w, m, a.ec.c20});
                 ++c_valid;
                 c_sla += sc.sla;
                 consider(r0, r1, sc, a.index_base + i, a.select_mode);
@@ -127,12 +155,11 @@ __global__ void __launch_bounds__(SNT) score_graphs_kernel(const __grid_constant
 // while the CTA scores the current one.  Per candidate: exact fp64 FMAs of the
 // three per-edge rows (integers < 2^53: exact in any order, = the int64 sums),
 // slice counts and the latency-rank presence mask; the idle row is per slice,
-// so S_idle = sum_s count_s * idle_s after the loop.
+// so S_idle = sum_s count_s * idle_s after the loop.  The p95 walk reads the
+// candidate's weights back from the staged tile.
 constexpr int GS = 3;                       // pipeline stages
 constexpr int CPT = 2;                      // candidates per thread
 constexpr int GT = SNT * CPT;               // candidates per tile
-constexpr int PCH = 7;                      // presence-mask chunk (bits)
-constexpr int NPCH = (CLV_MAX_EDGES + PCH - 1) / PCH;
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
     return (unsigned)__cvta_generic_to_shared(p);
@@ -159,33 +186,19 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
 struct GraphRows {
     double thr[CLV_MAX_EDGES], acc[CLV_MAX_EDGES], en[CLV_MAX_EDGES];
     double idle[CLV_K];
-    unsigned long long bad;                 // bit e: edge e is memory-infeasible
+    unsigned long long bad;                 // bit rank(e): edge e is memory-infeasible
+    unsigned char rk[CLV_MAX_EDGES];        // latency rank of edge e
 };
 
-// The p95 of a graph is the largest lat95 over its present edges: the present-edge
-// mask is split into 7-bit chunks and each chunk's maximum comes from a 128-entry
-// table (shared memory), so the per-edge work is one predicate-set bit.
 template <int V, bool FAST>
 __global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_constant__ ScoreArgs a,
                                                                const __grid_constant__ GraphRows R) {
     constexpr int E = V * CLV_K;
-    constexpr int NC = (E + PCH - 1) / PCH;
     extern __shared__ __align__(128) unsigned char gsm[];
     __shared__ __align__(8) unsigned long long full[GS];
-    __shared__ double chunk_max[NC][1 << PCH];
+    __shared__ RankTabs rt;
     uint16_t *ring = reinterpret_cast<uint16_t *>(gsm);
-    {
-        const FamilyTables &T = *a.fam;
-        for (int q = threadIdx.x; q < NC * (1 << PCH); q += SNT) {
-            const int c = q >> PCH, bits = q & ((1 << PCH) - 1);
-            double mx = 0.0;
-            for (int b = 0; b < PCH; ++b) {
-                const int e = c * PCH + b;
-                if (e < E && ((bits >> b) & 1)) mx = mx > T.lat95[e] ? mx : T.lat95[e];
-            }
-            chunk_max[c][bits] = mx;
-        }
-    }
+    stage_ranks(rt, *a.fam);
     if (threadIdx.x == 0) {
         for (int q = 0; q < GS; ++q) mbar_init(&full[q], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -246,7 +259,7 @@ __global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_cons
                 S1[c] = __fma_rn(xd, R.acc[e], S1[c]);
                 S2[c] = __fma_rn(xd, R.en[e], S2[c]);
                 sv[c][e % CLV_K] += x;
-                pe[c] |= (unsigned long long)(x != 0) << e;
+                pe[c] |= (unsigned long long)(x != 0) << R.rk[e];
             }
         }
 #pragma unroll
@@ -256,18 +269,13 @@ __global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_cons
             double S3 = 0.0;
 #pragma unroll
             for (int k = 0; k < CLV_K; ++k) S3 = __fma_rn((double)sv[c][k], R.idle[k], S3);
-            double lmax = 0.0;
-#pragma unroll
-            for (int q = 0; q < NC; ++q) {
-                const double v = chunk_max[q][(pe[c] >> (q * PCH)) & ((1 << PCH) - 1)];
-                lmax = lmax > v ? lmax : v;
-            }
             const long long i = tile * GT + local;
             const bool feas = !(pe[c] & R.bad) && pe[c] != 0 &&
                               feasible(a.F, n, sv[c][0], sv[c][1], sv[c][2], sv[c][3], sv[c][4]);
             if (feas) {
-                Score sc = epilogue_t<FAST>(S0[c], S1[c], S2[c], S3, lmax,
-                                      (double)(sv[c][0] + sv[c][1] + sv[c][2] + sv[c][3] + sv[c][4]), a.ec);
+                Score sc = epilogue_t<FAST>(S0[c], S1[c], S2[c], S3,
+                                            (double)(sv[c][0] + sv[c][1] + sv[c][2] + sv[c][3] + sv[c][4]), a.ec,
+                                            EdgeWalk<uint16_t>{&rt, w0 + c * SNT * E, pe[c], a.ec.c20});
                 ++c_valid;
                 c_sla += sc.sla;
                 consider(r0, r1, sc, a.index_base + i, a.select_mode);
@@ -311,7 +319,8 @@ cudaError_t launch_score_graphs(const ScoreArgs &a, const FamilyTables &T, int g
         GraphRows R{};
         for (int e = 0; e < T.E; ++e) {
             R.thr[e] = (double)T.thr_q[e]; R.acc[e] = (double)T.acc_q[e]; R.en[e] = (double)T.en_q[e];
-            if (!((T.mem_ok >> e) & 1ULL)) R.bad |= 1ULL << e;
+            R.rk[e] = T.rank[e];
+            if (!((T.mem_ok >> e) & 1ULL)) R.bad |= 1ULL << T.rank[e];
         }
         for (int k = 0; k < CLV_K; ++k) R.idle[k] = (double)T.idle_q[k];
         switch (T.V) {
@@ -342,8 +351,9 @@ cudaError_t launch_score_graphs(const ScoreArgs &a, const FamilyTables &T, int g
 // (counts laid out [bucket][thread]: conflict-free); the rows -- one 16-B int4 of the
 // fixed-point values, each < 2^31 -- are applied once per edge after the walk
 // (S = sum_e count_e * row_e, exact int64), which also yields the presence mask for
-// the p95 term and the memory-fit check.  Rows longer than 65,535 slots take the
-// direct per-slot sum.
+// the p95 term and the memory-fit check; the p95 walk then reads the counts of the
+// ranks it visits.  Rows longer than 65,535 slots take the direct per-slot sum (and
+// recount the visited edges from the row).
 //
 // Validation follows FleetConfig.__init__ (mig.py:248-263) then the SPEC's evaluation
 // (SPEC:267-275): an unknown partition id anywhere in the row -> InvalidConfigError;
@@ -392,11 +402,10 @@ __device__ __forceinline__ void walk_row(unsigned short *hc, const uint8_t *xpr,
             m |= 1ULL << (ro & 63);
         }
     }
-    if (HIST) {                                        // apply the rows; leave the counts zeroed
+    if (HIST) {                                        // apply the rows (the caller zeroes the counts)
         const int NB = 5 * (V + 2);
         for (int b = 0; b < NB; ++b) {
             const unsigned c = hc[b * XT];
-            hc[b * XT] = 0;
             if (b < 5) { lt1 |= c != 0; continue; }
             if (b >= 5 * (V + 1)) { infeas |= c != 0; continue; }
             const int4 R = row[b - 5];
@@ -418,11 +427,31 @@ __device__ __forceinline__ void walk_row(unsigned short *hc, const uint8_t *xpr,
         : infeas ? CLV_ERR_INFEASIBLE_ASSIGNMENT : 0;
 }
 
+// Slots of a row that land on edge e (the long-row path keeps no per-edge counts).
+__device__ inline int count_edge_slots(const uint8_t *xpr, const uint8_t *xvr, int mcnt, int n, const unsigned *cfg,
+                                       int e) {
+    int g = 0, left = 0, cntv = 0;
+    unsigned kw = 0;
+    for (int p = 0; p < mcnt; ++p) {
+        if (left == 0) {
+            const unsigned c = cfg[__ldg(xpr + min(g, n - 1))];
+            const int ns = (c >> 24) & 15;
+            left = ns > 0 ? ns : 1;
+            kw = c; ++g;
+        }
+        const int v = __ldg(xvr + p);
+        const int kind = kw & 7;
+        kw >>= 3; --left;
+        cntv += (v >= 1 && (v - 1) * 5 + kind == e);
+    }
+    return cntv;
+}
+
 template <bool FAST>
 __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ ScoreArgs a, int n, int xp_stride,
                                                      int xv_cap) {
     __shared__ int4 row[CLV_MAX_EDGES];
-    __shared__ double lat_by_rank[CLV_MAX_EDGES];
+    __shared__ RankTabs rt;
     __shared__ unsigned char rank_ok[CLV_MAX_EDGES];   // 0x40 | rank when memory-feasible, else 0
     __shared__ unsigned cfg[256];
     __shared__ unsigned short hist[(CLV_MAX_EDGES + 10) * XT];  // [bucket][thread] slot counts of the row
@@ -435,9 +464,9 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
         const bool live = e < T.E;
         row[e] = live ? make_int4((int)T.thr_q[e], (int)T.acc_q[e], (int)T.en_q[e], (int)T.idle_q[e % 5])
                       : make_int4(0, 0, 0, 0);
-        lat_by_rank[e] = live ? T.lat_by_rank[e] : 0.0;
         rank_ok[e] = (live && ((T.mem_ok >> e) & 1ULL)) ? (unsigned char)(0x40 | T.rank[e]) : 0;
     }
+    stage_ranks(rt, T);
     for (int t = threadIdx.x; t < 256; t += XT) cfg[t] = 0u;
     for (int q = threadIdx.x; q < (CLV_MAX_EDGES + 10) * XT; q += XT) hist[q] = 0;
     __syncthreads();
@@ -493,13 +522,15 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
             long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
             unsigned long long m = 0;
             int err;
+            unsigned short *hc = hist + threadIdx.x;
+            const uint8_t *gxr = a.xv + o0, *gxpr = a.xp + c * n;
+            const bool long_row = o1 - o0 > 0xFFFF;
             if (o1 - o0 < 0 || o1 - o0 > 0x7FFFFFFFLL) {
                 err = CLV_ERR_CARBON_SCHED;
             } else {
                 const int mcnt = (int)(o1 - o0);
-                const uint8_t *sxr = sxv + lead + (o0 - G0), *gxr = a.xv + o0;
-                const uint8_t *sxpr = sxp + threadIdx.x * xp_stride, *gxpr = a.xp + c * n;
-                unsigned short *hc = hist + threadIdx.x;
+                const uint8_t *sxr = sxv + lead + (o0 - G0);
+                const uint8_t *sxpr = sxp + threadIdx.x * xp_stride;
                 if (mcnt > 0xFFFF)
                     walk_row<false, false, false>(hc, gxpr, gxr, mcnt, n, V, cfg, row, rank_ok, S0, S1, S2, S3, m, err);
                 else if (xp_stride && xv_fits)
@@ -513,8 +544,14 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
                 atomicMin(a.error_key, ((unsigned long long)c << 8) | (unsigned)err);
                 if (a.sla_out) a.sla_out[c] = 0;
             } else {
-                Score sc = epilogue_t<FAST>((double)S0, (double)S1, (double)S2, (double)S3,
-                                            lat_by_rank[63 - __clzll((long long)m)], (double)(o1 - o0), a.ec);
+                const int mc = (int)(o1 - o0);
+                Score sc = epilogue_t<FAST>((double)S0, (double)S1, (double)S2, (double)S3, (double)mc, a.ec,
+                                            [&](double W0) {
+                    return p95_walk(m, W0, a.ec.c20, rt.svc, rt.lat, [&](int r) {
+                        const int e = rt.edge[r];
+                        return (double)(long_row ? count_edge_slots(gxpr, gxr, mc, n, cfg, e) : hc[(e + 5) * XT]);
+                    });
+                });
                 ++c_valid;
                 c_sla += sc.sla;
                 consider(r0, r1, sc, a.index_base + c, a.select_mode);
@@ -522,6 +559,8 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
                 if (a.h_out) a.h_out[c] = sc.h;
                 if (a.sla_out) a.sla_out[c] = sc.sla;
             }
+            if (!long_row)
+                for (int b = 0; b < 5 * (V + 2); ++b) hc[b * XT] = 0;
         }
     }
     grid_finish<XT>(r0, r1, c_valid, c_sla, a.sel);
@@ -550,12 +589,11 @@ cudaError_t launch_score_x(const ScoreArgs &a, int n, int max_grid, cudaStream_t
 template <bool FAST>
 __global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ OracleArgs a) {
     __shared__ ERow row[CLV_MAX_EDGES];
-    __shared__ double lat_by_rank[CLV_MAX_EDGES];
-    __shared__ unsigned char rank[CLV_MAX_EDGES];
+    __shared__ RankTabs rt;
     __shared__ unsigned char flist[CLV_K][CLV_MAX_VARIANTS];
     const FamilyTables &T = *a.fam;
     const Topology &P = *a.topo;
-    stage_rows(row, lat_by_rank, rank, T);
+    stage_rows(row, rt, T);
     for (int t = threadIdx.x; t < CLV_K * CLV_MAX_VARIANTS; t += SNT)
         flist[t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS] = T.feas_list[t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS];
     __syncthreads();
@@ -571,6 +609,7 @@ __global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ Ora
         long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
         unsigned long long m = 0;
         const int ns = P.nslices[r];
+        unsigned long long rks = 0;                // latency rank of slice j in byte j
         for (int j = 0; j < ns; ++j) {
             const unsigned pl = (unsigned)a.row_place[r][j];
             const int dgt = (int)(rem / pl);
@@ -578,10 +617,18 @@ __global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ Ora
             const int k = P.kinds[r][j];
             const int e = flist[k][dgt] * 5 + k;
             S0 += row[e].thr; S1 += row[e].acc; S2 += row[e].en; S3 += row[e].idle;
-            m |= 1ULL << rank[e];
+            m |= 1ULL << rt.rank[e];
+            rks |= (unsigned long long)rt.rank[e] << (8 * j);
         }
+        const double nd = (double)n;
         Score sc = epilogue_t<FAST>((double)(S0 * n), (double)(S1 * n), (double)(S2 * n), (double)(S3 * n),
-                                    lat_by_rank[63 - __clzll((long long)m)], (double)(n * ns), a.ec);
+                                    (double)(n * ns), a.ec, [&](double W0) {
+            return p95_walk(m, W0, a.ec.c20, rt.svc, rt.lat, [&](int rr) {
+                int c = 0;
+                for (int j = 0; j < ns; ++j) c += (int)((rks >> (8 * j)) & 0xFF) == rr;
+                return (double)c * nd;             // exact: the standardized graph is n x the row
+            });
+        });
         ++c_valid;
         c_sla += sc.sla;
         consider(r0, r1, sc, i, CLV_SELECT_ORACLE);
@@ -635,7 +682,7 @@ template <bool FAST, bool HIST>
 __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ SweepArgs a) {
     __shared__ SRow row[CLV_MAX_PODS][CLV_MAX_EDGES + 1];
     __shared__ unsigned long long rbit[CLV_MAX_PODS][CLV_MAX_EDGES + 1];
-    __shared__ double lat_by_rank[CLV_MAX_PODS][CLV_MAX_EDGES];
+    __shared__ RankTabs rt[CLV_MAX_PODS];
     __shared__ unsigned char nfeas[CLV_MAX_PODS][CLV_K];
     __shared__ unsigned char flist[CLV_MAX_PODS][CLV_K][CLV_MAX_VARIANTS];
     __shared__ unsigned char nsl[CLV_MAX_CONFIGS];
@@ -653,8 +700,8 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
             row[p][e].en = real ? (double)T.en_q[e] : 0.0;
             row[p][e].idle = real ? (double)T.idle_q[e % 5] : 0.0;
             rbit[p][e] = real ? (1ULL << T.rank[e]) : 0ULL;
-            if (e < CLV_MAX_EDGES) lat_by_rank[p][e] = T.lat_by_rank[e];
         }
+        stage_ranks(rt[p], T);
         for (int t = threadIdx.x; t < CLV_K * CLV_MAX_VARIANTS; t += SNT) {
             flist[p][t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS] = T.feas_list[t / CLV_MAX_VARIANTS][t % CLV_MAX_VARIANTS];
             if (t < CLV_K) nfeas[p][t] = T.nfeas[t];
@@ -692,6 +739,7 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
             // slice's variant draw.  The body is branch-free (a configuration draw adds the
             // all-zero row), so lanes stay converged until their last GPU.
             const int ng = a.pods[p].n_gpus;
+            const Draws d0 = d;                          // the pod's first draw (recount path)
             int g = 0, rem = 0, r = 0, slot = 0, inst = 0;
             if (HIST) {
                 unsigned nfw = 0;                        // per-kind feasible-variant counts, 4 bits each
@@ -714,14 +762,12 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
                 const int E = pod_e[p];
                 for (int e = 0; e < E; ++e) {
                     const unsigned c = hc[e * SNT];
-                    hc[e * SNT] = 0;
                     const double cd = (double)c;
                     const SRow &q = row[p][e];
                     S0 = __fma_rn(cd, q.thr, S0); S1 = __fma_rn(cd, q.acc, S1);
                     S2 = __fma_rn(cd, q.en, S2); S3 = __fma_rn(cd, q.idle, S3);
                     m |= c ? rbit[p][e] : 0ULL;
                 }
-                hc[ZROW * SNT] = 0;
             } else {
                 while (rem != 0 || g < ng) {
                     const uint32_t w = d.next();
@@ -740,8 +786,33 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
                     inst += cfg ? 0 : 1;
                 }
             }
-            Score sc = epilogue_t<FAST>(S0, S1, S2, S3, lat_by_rank[p][63 - __clzll((long long)m)], (double)inst,
-                                  a.pods[p].ec);
+            // the p95 walk reads the visited edges' counts (HIST), or recounts them by
+            // replaying the pod's draws (pods with 7 n >= 2^16)
+            Score sc = epilogue_t<FAST>(S0, S1, S2, S3, (double)inst, a.pods[p].ec, [&](double W0) {
+                return p95_walk(m, W0, a.pods[p].ec.c20, rt[p].svc, rt[p].lat, [&](int rr) {
+                    const int e0 = rt[p].edge[rr];
+                    if (HIST) return (double)hc[e0 * SNT];
+                    Draws dd = d0;
+                    int gg = 0, rm = 0, rw = 0, sl = 0, cntv = 0;
+                    while (rm != 0 || gg < ng) {
+                        const uint32_t w = dd.next();
+                        const bool cf = rm == 0;
+                        const int k = kinds[rw][sl & 7];
+                        const int v = flist[p][k][(int)(((uint64_t)w * nfeas[p][k]) >> 32)];
+                        cntv += (!cf && v * 5 + k == e0);
+                        const int rn = (int)(((uint64_t)w * K) >> 32);
+                        rw = cf ? rn : rw;
+                        rm = cf ? (int)nsl[rn] : rm - 1;
+                        sl = cf ? 0 : sl + 1;
+                        gg += cf ? 1 : 0;
+                    }
+                    return (double)cntv;
+                });
+            });
+            if (HIST) {
+                for (int e = 0; e < pod_e[p]; ++e) hc[e * SNT] = 0;
+                hc[ZROW * SNT] = 0;
+            }
             const double wt = a.pods[p].weight;
             if (p == 0) { f = wt * sc.f; h = wt * sc.h; }
             else { f = f + wt * sc.f; h = h + wt * sc.h; }

@@ -162,9 +162,10 @@ class CloverEngine:
         arr = lambda x, dt: np.ascontiguousarray(np.asarray(x, dtype=dt))
         thr, acc, en, idle = arr(t.thr_q, np.int64), arr(t.acc_q, np.int64), arr(t.en_q, np.int64), arr(t.idle_q, np.int64)
         lat, mem = arr(t.lat95, np.float64), arr(t.mem_ok, np.uint8)
+        svc = arr(t.svc_ms, np.float64)
         self._check(self.lib.clv_set_profile(self.ctx, fam, t.variant_count, thr.ctypes.data, acc.ctypes.data,
-                                             en.ctypes.data, idle.ctypes.data, lat.ctypes.data, mem.ctypes.data,
-                                             t.kt, t.ke, t.ki))
+                                             en.ctypes.data, idle.ctypes.data, lat.ctypes.data, svc.ctypes.data,
+                                             mem.ctypes.data, t.kt, t.ke, t.ki))
         try:
             self._set_sim_profile(fam, profile)
             sim_error = None

@@ -280,6 +280,7 @@ class ScoringTables:
     en_q[e]   = round(thr(e) * energy(e) * 2^ke)  (Wh/s)
     idle_q[s] = round(idle_w(s) * 2^ki)          (W)
     lat95[e]  = p95 service time (ms), fp64
+    svc_ms[e] = mean service time (ms): request shares of the p95 walk
     mem_ok[e] = memory feasibility of the edge
     Each row is < 2^31, so sums over up to 2^21 instances are exact in int64
     and convert exactly to fp64.
@@ -297,6 +298,7 @@ class ScoringTables:
     ke: int
     ki: int
     thr: np.ndarray = field(repr=False)
+    svc_ms: np.ndarray = field(repr=False, default=None)
 
     @property
     def n_edges(self) -> int:
@@ -330,8 +332,10 @@ class ScoringTables:
                           dtype=np.int64)
         if np.any(thr_q <= 0):
             raise ProfileError("throughput underflows the fixed-point scale")
+        svc = [p.service[(v, s)].mean_service_ms for v in range(1, V + 1) for s in SLICE_ORDER]
         return cls(p.name, V, thr_q, acc_q, en_q, idle_q, np.array(lat, dtype=np.float64),
-                   np.array(mem, dtype=bool), kt, ke, ki, np.array(thr, dtype=np.float64))
+                   np.array(mem, dtype=bool), kt, ke, ki, np.array(thr, dtype=np.float64),
+                   np.array(svc, dtype=np.float64))
 
 
 # ---------------------------------------------------------------------------

@@ -74,7 +74,7 @@ def test_reference_style_ctypes_binding_runs_the_oracle(engine):
         f64 = lambda xs: (ctypes.c_double * len(xs))(*[float(x) for x in xs])
         u8 = lambda xs: (ctypes.c_uint8 * len(xs))(*[int(x) for x in xs])
         assert lib.clv_set_profile(ctx, 0, t.variant_count, i64(t.thr_q), i64(t.acc_q), i64(t.en_q), i64(t.idle_q),
-                                   f64(t.lat95), u8(t.mem_ok), t.kt, t.ke, t.ki) == 0
+                                   f64(t.lat95), f64(t.svc_ms), u8(t.mem_ok), t.kt, t.ke, t.ki) == 0
         sc = engine.calibrate(prof, 1, 400.0, 0.5)
         o = sc.obj
         p = EvalParams(sc.arrival_rps, sc.ci, o.carbon_weight, o.base_accuracy, o.base_carbon_g, o.latency_slo_ms,
@@ -116,7 +116,7 @@ def test_reference_style_ctypes_binding_replans(engine):
         f64 = lambda xs: (ctypes.c_double * len(xs))(*[float(x) for x in xs])
         u8 = lambda xs: (ctypes.c_uint8 * len(xs))(*[int(x) for x in xs])
         assert lib.clv_set_profile(ctx, 0, t.variant_count, i64(t.thr_q), i64(t.acc_q), i64(t.en_q), i64(t.idle_q),
-                                   f64(t.lat95), u8(t.mem_ok), t.kt, t.ke, t.ki) == 0
+                                   f64(t.lat95), f64(t.svc_ms), u8(t.mem_ok), t.kt, t.ke, t.ki) == 0
         sc = engine.calibrate(prof, 64, 350.0, 0.5)
         o = sc.obj
         p = EvalParams(sc.arrival_rps, sc.ci, o.carbon_weight, o.base_accuracy, o.base_carbon_g, o.latency_slo_ms,
