@@ -4,8 +4,10 @@
 Default workload (BASELINE.json configs[2], the multi-GPU one; per-GPU share at
 N GPUs, weak scaling): a 64-GPU fleet, EfficientNet B1-B7 catalog (V=7),
 lambda=0.5, 128 independent annealing chains per B200 (1024 on 8), each from a
-random realizable start, full GED<=4 neighbourhood scored every step, run to
-termination (stall 5 / 64 steps).  One bench step = one complete re-plan of all
+perturbation of the incumbent deployment (a re-plan starts from the
+incumbent; each GPU keeps BASE's partition with probability 0.75, else a BLOVER
+redraw), full GED<=4 neighbourhood scored every step, run to termination (stall 5,
+<= 256 steps: the chains converge by the stall rule).  One bench step = one complete re-plan of all
 chains (so ms_per_step is the per-re-plan time-to-solution) followed by the
 per-round winner exchange (NCCL all_gather of 32-byte records when N > 1).
 
@@ -51,10 +53,12 @@ def parse():
     ap.add_argument("--impl", default="clover", choices=["clover", "reference"])
     ap.add_argument("--chains", type=int, default=CHAINS_PER_GPU)
     ap.add_argument("--cluster", type=int, default=0, help="CTAs per chain (0 = auto: one wave)")
-    ap.add_argument("--max-steps", type=int, default=64)
+    ap.add_argument("--max-steps", type=int, default=256)
+    ap.add_argument("--keep", type=float, default=0.75, help="c2 starts: P(GPU keeps the incumbent partition)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-replan", action="store_true", help="skip the all-core CPU re-plan (TTS + parity)")
     ap.add_argument("--workload", default="c2", choices=["c0", "c1", "c2", "c3", "c4", "des"],
                     help="c2 (default) is the headline; c0/c1/c4 are the other BASELINE configs")
     ap.add_argument("--sweep", type=int, default=1_000_000_000, help="c4: candidates per sweep (whole job)")
@@ -73,10 +77,12 @@ def anneal_params(max_steps):
     return AnnealParams(max_steps=max_steps, stall_limit=5, proposal="best", evaluate="all")
 
 
-def make_starts(engine, profile, seed, first, count):
-    from paper_2304_09781_b200.search import random_fleets
+def make_starts(profile, seed, first, count, keep):
+    """c2 start graphs: perturbations of the incumbent (BASE) deployment, host-side draws
+    (search.perturbed_fleets), identical for the GPU arm, the CPU legs and the parity check."""
+    from paper_2304_09781_b200.search import base_config, perturbed_fleets
     from paper_2304_09781_b200.graph import build_graph
-    fleets = random_fleets(engine, profile, N_FLEET, seed, count, first)
+    fleets = perturbed_fleets(base_config(N_FLEET, profile), profile, seed, count, first, keep)
     return np.array([build_graph(f, profile).weights for f in fleets], dtype=np.uint16)
 
 
@@ -169,7 +175,7 @@ def _cpu_chain(args):
     from oracle.anneal import anneal_chain
     t0 = time.perf_counter()
     out = anneal_chain(w0, N_FLEET, _CPU["T"], _CPU["sc"], anneal_params(max_steps), seed, chain, _CPU["feas"])
-    return out.evals, time.perf_counter() - t0
+    return out.evals, time.perf_counter() - t0, out
 
 
 _CPU = {}
@@ -200,20 +206,64 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_baseline(starts, seed, max_steps, seconds):
-    """Oracle port on one host core over a bounded sample of the same chains."""
+def chain_parity(outs, gpu_batch):
+    """Bit-for-bit comparison of oracle chains with the GPU's results for the same chains."""
+    h = gpu_batch.host()
+    u64 = lambda x: np.float64(x).view(np.uint64)
+    bad = []
+    for c, out in enumerate(outs):
+        r = h["results"][c]
+        same = (int(r["status"]) == out.status and int(r["steps"]) == out.steps and int(r["evals"]) == out.evals
+                and int(r["best_step"]) == out.best_step and int(r["best_index"]) == out.best_idx
+                and np.array_equal(h["best_w"][c].astype(np.int64), out.best_w)
+                and np.array_equal(h["final_w"][c].astype(np.int64), out.final_w)
+                and u64(r["f"]) == u64(out.best["f"]) and u64(r["h"]) == u64(out.best["h"])
+                and u64(r["p95_ms"]) == u64(out.best["L"]) and bool(r["sla_met"]) == bool(out.best["sla"]))
+        if not same:
+            bad.append(c)
+    return {"chains": len(outs), "bit_exact": not bad, "mismatched_chains": bad,
+            "compared": "status, steps, evals, best_step, best_index, best_w, final_w, f/h/p95 bits, sla_met "
+                        "of the GPU's first timed batch vs oracle/anneal.py (same starts, seed, chain ids)"}
+
+
+def cpu_replan(starts, seed, max_steps):
+    """The same re-plan (every chain of one bench step) by the oracle port on all host cores:
+    a measured CPU time-to-solution, and the chains for the parity check."""
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    _cpu_setup(None)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_chain, [(starts[c].astype(np.int64), c, seed, max_steps) for c in range(len(starts))],
+                       chunksize=1)
+        wall = time.perf_counter() - t0
+    evals = sum(r[0] for r in res)
+    return {"replan_tts_cpu_s": wall, "cores": cores, "chains": len(starts), "candidates": evals,
+            "value": evals / wall, "unit": UNIT, "kind": "port", "cpu_model": cpu_model()}, [r[2] for r in res]
+
+
+def cpu_baseline(starts, seed, max_steps, seconds, gpu_batch=None, min_chains=16):
+    """Oracle port on one host core over a bounded sample of the same chains.  The same
+    oracle runs double as the parity check of the timed batch: every sampled chain's
+    status, steps, evaluation count, best step / index, best graph and f / h / p95 bits
+    are compared with the GPU's results for that chain of the same bench step."""
     _cpu_setup(None)
     evals, spent, chains = 0, 0.0, 0
+    outs = []
     for c in range(len(starts)):
-        e, t = _cpu_chain((starts[c].astype(np.int64), c, seed, max_steps))
+        e, t, out = _cpu_chain((starts[c].astype(np.int64), c, seed, max_steps))
         evals += e
         spent += t
         chains += 1
-        if spent >= seconds:
+        outs.append(out)
+        if spent >= seconds and chains >= min_chains:
             break
-    return {"value": evals / spent, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
-            "sample": "%d of the step-0 chains (n=%d, V=7) annealed to termination by oracle/anneal.py, "
-                      "%d candidates in %.1f s" % (chains, N_FLEET, evals, spent)}
+    cpu = {"value": evals / spent, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
+           "sample": "%d of the first timed step's chains (n=%d, V=7) annealed to termination by oracle/anneal.py, "
+                     "%d candidates in %.1f s" % (chains, N_FLEET, evals, spent)}
+    parity = chain_parity(outs, gpu_batch) if gpu_batch is not None else None
+    return cpu, parity
 
 
 def run_reference(args, rank, world):
@@ -224,7 +274,7 @@ def run_reference(args, rank, world):
     cores = len(os.sched_getaffinity(0))
     _cpu_setup(None)
     prof = synthetic_profile(FAMILY)
-    starts = _reference_starts(prof, (args.warmup + args.steps) * cores)
+    starts = make_starts(prof, SEED, 0, (args.warmup + args.steps) * cores, args.keep)
     ctx = mp.get_context("fork")
     total_evals, total_time = 0, 0.0
     with ctx.Pool(cores) as pool:
@@ -241,31 +291,20 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * total_time / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": _config(args, world),
+            "config": _config(args, world, cores_chains=cores),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                              "sample": "%d chains per step (one per core), n=%d, V=7, oracle/anneal.py" % (cores, N_FLEET)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def _reference_starts(prof, count):
-    """Same counter-RNG draws as the GPU arm, decoded by the oracle (no GPU here)."""
-    from oracle.search import Pod, draw_candidate, fleet_graph
-    from paper_2304_09781_b200.mig import DEFAULT_TOPOLOGY
-    T = _CPU["T"]
-    out = []
-    for i in range(count):
-        (parts, assign), = draw_candidate(SEED, i, [Pod(T, None, N_FLEET, 1.0)], DEFAULT_TOPOLOGY)
-        out.append(fleet_graph(parts, assign, DEFAULT_TOPOLOGY, T))
-    return np.array(out, dtype=np.uint16)
-
-
 def _config(args, world, cores_chains=None):
     return {"workload": "c2: n=%d-GPU fleet, %s B1-B7 (V=7), lambda=%.1f, ci=%.0f gCO2/kWh, %d annealing chains "
-                        "per B200 from random realizable starts, full GED<=4 neighbourhood scored per step, "
-                        "run to termination (stall 5, <=%d steps); one step = one re-plan of all chains"
+                        "per %s from perturbations of the incumbent (BASE) deployment (keep %.2f), full GED<=4 "
+                        "neighbourhood scored per step, run to termination (stall 5, <=%d steps); one step = one "
+                        "re-plan of all chains"
                         % (N_FLEET, FAMILY, LAMBDA, CI, args.chains if cores_chains is None else cores_chains,
-                           args.max_steps),
+                           "B200" if cores_chains is None else "CPU step", args.keep, args.max_steps),
             "fleet_gpus": N_FLEET, "variants": 7, "chains_per_gpu": args.chains if cores_chains is None else cores_chains,
             "chains_total": (args.chains * world) if cores_chains is None else cores_chains,
             "proposal": "best-h neighbour", "parallelism": "chains sharded across %d GPU(s), dp%d" % (world, world),
@@ -306,7 +345,7 @@ def main():
     total_steps = args.warmup + args.steps
     base = rank * C
     # chains of step s, rank r are candidates [s*C*world + r*C, ...) of the counter-RNG stream
-    starts = [make_starts(eng, prof, SEED, s * C * world + base, C) for s in range(total_steps)]
+    starts = [make_starts(prof, SEED, s * C * world + base, C, args.keep) for s in range(total_steps)]
     starts_dev = [torch.from_numpy(x.view(np.int16)).cuda().view(torch.uint16) for x in starts]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
@@ -421,9 +460,24 @@ def main():
                            "candidates per launch (the kernel scores incrementally: ~12 DADD + epilogue)"
                            % (edge_evals / max(evals, 1), per_launch_cand),
             "anneal_share_of_step": sum(anneal_ms) / sum(step_ms)}
-    cpu = None
+    cpu, parity, cpu_tts = None, None, None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(starts[args.warmup], SEED + args.warmup, args.max_steps, args.cpu_seconds)
+        cpu, parity = cpu_baseline(starts[args.warmup], SEED + args.warmup, args.max_steps, args.cpu_seconds,
+                                   gpu_batch=batches[args.warmup])
+        if not args.no_cpu_replan:
+            cpu_tts, outs = cpu_replan(starts[args.warmup], SEED + args.warmup, args.max_steps)
+            parity = chain_parity(outs, batches[args.warmup])
+    # re-plan quality of the timed batches: SLA-meeting winners and how the chains ended
+    hs = [batches[s].host()["results"] for s in range(args.warmup, total_steps)]
+    allr = np.concatenate(hs)
+    quality = {"chains": int(len(allr)),
+               "chain_winners_sla_met": float(np.mean(allr["sla_met"] != 0)),
+               "replan_winner_sla_met": float(np.mean([bool(r["sla_met"][np.lexsort((np.arange(len(r)), r["h"],
+                                                                                       r["sla_met"] == 0))[0]])
+                                                       for r in hs])),
+               "status": {"max_steps": int(np.sum(allr["status"] == 0)), "stalled": int(np.sum(allr["status"] == 1)),
+                          "no_neighbour": int(np.sum(allr["status"] == 2))},
+               "steps_quantiles": {q: int(np.quantile(allr["steps"], float(q))) for q in ("0.1", "0.5", "0.9", "1.0")}}
     launches_per_step = 2 + (1 if world > 1 else 0)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * dev_time / args.steps, "higher_is_better": True,
@@ -435,8 +489,7 @@ def main():
                              "search.anneal_chains -> clv_anneal + clv_select_chains + record all-gather + D2H")},
             "gpu_launches": launches_per_step * args.steps, "roofline": roof, "cpu_baseline": cpu,
             "replan_tts_ms": 1000.0 * dev_time / args.steps,
-            "replan_tts_cpu_s": (None if cpu is None else (evals_all / args.steps) / cpu["value"]),
-            "replan_tts_cpu_note": "candidates per re-plan / measured 1-core oracle rate (same chains, same algorithm)",
+            "replan_tts_cpu": cpu_tts, "parity": parity, "replan_quality": quality,
             "chain_steps_per_replan": chain_steps_all / args.steps,
             "wall_s_timed_region": t_wall}
     print(json.dumps(line), flush=True)

@@ -4,10 +4,11 @@ Restates DESIGN.md "Scoring surrogate" (the replacement for SPEC:334-372's DES,
 SURVEY 7.2 D1) and Eqs. 1, 2, 3, 6 in numpy.  The p95 term is the
 nearest-rank p95 over requests of the fleet's service-time mixture:
 request shares follow the instance-pull dispatch of SPEC:335 at utilisation
-rho < 1 (every instance waits W0 = (1000 m / R)(1 - rho) ms in the idle queue
-between services, so instance j serves 1000 / (s_j + W0) requests/s; W0 -> 0
-gives SPEC:390's throughput shares under saturation), walked from the slowest
-edge down until the tail holds more than 5 % of the arrival rate R.  Eq. 1 / Eq. 2 use
+rho < 1 (every instance waits W ms in the idle queue between services, so instance j
+serves 1 / (s_j + W) requests/s, W the root of "the instances' rates sum to R" over a
+2-point Gauss quadrature of the fleet's service rates; W = 0 gives SPEC:390's
+throughput shares under saturation), walked from the slowest edge down until the
+tail carries more than 5 % of R.  Eq. 1 / Eq. 2 use
 the algebraically identical forms (A - A_base) * (100 / A_base) and
 100 - E * (ci / (10 C_base)); tests pin them to the SPEC-literal quotients.
 Aggregates are recomputed from scratch per candidate (W @ rows, int64), so this
@@ -41,7 +42,7 @@ def constants(tables: OracleTables, scenario):
     return dict(R_q=math.ldexp(R, tables.kt), inv_3600R=1.0 / (3600.0 * R),
                 en_scale=math.ldexp(1.0, tables.kt - tables.ke),
                 idle_scale=math.ldexp(1.0, -tables.ki),
-                kW=1000.0 / R, c20=20000.0 / R)
+                R=R, c20=20000.0 / R)
 
 
 def rank_order(tables: OracleTables) -> list:
@@ -49,14 +50,46 @@ def rank_order(tables: OracleTables) -> list:
     return sorted(range(tables.E), key=lambda e: (float(tables.lat95[e]), e))
 
 
-def p95_walk(W: np.ndarray, tables: OracleTables, W0: np.ndarray, c20: float) -> np.ndarray:
-    """Service p95 of each fleet (rows of W) given its idle-queue time W0 (ms).
+def idle_wait_ms(m, s1, s2, s3, R, R_q, inv, rho_c, tables):
+    """Idle-queue wait W (ms) of every fleet: the root of sum_j w_j x_j / (1 + W x_j) = R
+    (instance j serves 1 / (s_j + W) requests per second, x_j = 1 / s_j, the rates summing
+    to the arrival rate R) with the rate distribution replaced by its 2-point Gauss
+    quadrature (matching sum w x, sum w x^2, sum w x^3).  By Vieta the nodes drop out:
+    with a_k = sum w x^k, D = a2 m - a1^2, N0 = a1 a3 - a2^2, N1 = a1 a2 - a3 m the root
+    solves R N0 W^2 - (R N1 + m N0) W + (R - a1) D = 0 (the cancellation-free branch of the
+    quadratic formula).  Homogeneous fleets (D <= 1e-9 a2 m) and degenerate roots take
+    the homogeneous solution W = (m / R)(1 - rho); saturated fleets (rho >= 1) W = 0."""
+    t2, k2, t3, k3 = tables.rate_moment_rows()
+    a1 = s1 * math.ldexp(1.0, -tables.kt)
+    a2 = s2 * math.ldexp(1.0, -k2)
+    a3 = s3 * math.ldexp(1.0, -k3)
+    D = a2 * m - a1 * a1
+    N0 = a1 * a3 - a2 * a2
+    N1 = a1 * a2 - a3 * m
+    A = R * N0
+    B = -(R * N1) - m * N0
+    C = (R - a1) * D
+    with np.errstate(over="ignore", invalid="ignore", divide="ignore"):
+        x = B * B - (4.0 * A) * C
+        sq = np.sqrt(np.where(x > 0.0, x, 0.0))
+        num = np.where(B >= 0.0, -2.0 * C, sq - B)
+        den = np.where(B >= 0.0, B + sq, 2.0 * A)
+        root = num / np.where(den > 0.0, den, 1.0)
+        homo = (m * (1.0 / R)) * (1.0 - rho_c)
+        ok = (den > 0.0) & (root >= 0.0) & (root < np.inf) & ~(D <= (1e-9 * a2) * m)
+        W = np.where(ok, root, homo)
+        W = np.where(rho_c >= 1.0, 0.0, W)
+    return 1000.0 * W
 
-    Present edges are visited from the highest latency rank down; the tail's request
-    rate sum_j 1000 w_j / (s_j + W0) is kept as the fraction P / Q (no division):
-    d = s + W0, P <- P d + w Q, Q <- Q d; the walk stops at the first edge where
-    P * (20000 / R) > Q (the tail now holds > 5 % of R), else at the lowest present
-    edge.  The p95 is that edge's lat95."""
+
+def p95_walk(W: np.ndarray, tables: OracleTables, W0: np.ndarray, c20: float) -> np.ndarray:
+    """Service p95 of each fleet (rows of W) given its idle-queue wait W0 (ms).
+
+    Present edges are visited from the highest latency rank down; the tail's request rate,
+    scaled by c20 = 20000 / R, (20000 / R) sum_j w_j / (s_j + W0), is kept as the fraction
+    P / Q (no division): d = s + W0, P <- P d + (w c20) Q, Q <- Q d; the walk stops at the
+    first edge where P > Q (the tail now carries more than 5 % of the arrival rate R),
+    else at the lowest present edge.  The p95 is that edge's lat95."""
     W = np.asarray(W, dtype=np.int64).reshape(-1, tables.E)
     n = len(W)
     P = np.zeros(n)
@@ -69,12 +102,12 @@ def p95_walk(W: np.ndarray, tables: OracleTables, W0: np.ndarray, c20: float) ->
             if not act.any():
                 continue
             d = float(tables.mean_ms[e]) + W0
-            Pn = P * d + W[:, e].astype(np.float64) * Q
+            Pn = P * d + (W[:, e].astype(np.float64) * c20) * Q
             Qn = Q * d
             P = np.where(act, Pn, P)
             Q = np.where(act, Qn, Q)
             lq = np.where(act, float(tables.lat95[e]), lq)
-            done = done | (act & (P * c20 > Q))
+            done = done | (act & (P > Q))
     return lq
 
 
@@ -86,10 +119,12 @@ def aggregates(W: np.ndarray, tables: OracleTables):
     cnt = W.reshape(len(W), tables.V, 5).sum(axis=1)
     s_idle = cnt @ tables.idle_q
     m = W.sum(axis=1)
-    return s_thr, s_acc, s_en, s_idle, W, m
+    t2, _k2, t3, _k3 = tables.rate_moment_rows()
+    return s_thr, s_acc, s_en, s_idle, (W, W @ t2, W @ t3), m
 
 
-def epilogue(s_thr, s_acc, s_en, s_idle, W, m, tables, scenario) -> Evaluated:
+def epilogue(s_thr, s_acc, s_en, s_idle, walk_in, m, tables, scenario) -> Evaluated:
+    W, s2, s3 = walk_in
     c = constants(tables, scenario)
     obj = scenario.obj
     a_base, c_base, slo = obj.base_accuracy, obj.base_carbon_g, obj.latency_slo_ms
@@ -105,7 +140,8 @@ def epilogue(s_thr, s_acc, s_en, s_idle, W, m, tables, scenario) -> Evaluated:
         p_idle = s_idle.astype(np.float64) * c["idle_scale"]
         E = e_act + ((1.0 - rho_c) * p_idle) * c["inv_3600R"]
         md = np.asarray(m, dtype=np.float64)
-        W0 = (md * c["kW"]) * (1.0 - rho_c)           # idle-queue time between services (ms)
+        W0 = idle_wait_ms(md, s_thr.astype(np.float64), np.asarray(s2, dtype=np.float64),
+                          np.asarray(s3, dtype=np.float64), c["R"], c["R_q"], inv, rho_c, tables)
         lq = p95_walk(W, tables, W0, c["c20"])
         rho_q = np.minimum(rho, scenario.rho_sat)
         # queueing factor of m servers: L = lq * (1 + rho^8 / (m (1 - rho)))

@@ -42,6 +42,16 @@ class OracleTables:
     ki: int
     mean_ms: np.ndarray
 
+    def rate_moment_rows(self):
+        """(t2_q, k2, t3_q, k3): fixed-point rows of thr^2 and thr^3, thr = 1000 / mean_ms
+        (the second and third moments of the instance service rates)."""
+        thr = [1000.0 / float(x) for x in self.mean_ms]
+        t2 = [x * x for x in thr]
+        t3 = [y * x for x, y in zip(thr, t2)]
+        k2, k3 = _scale(max(t2)), _scale(max(t3))
+        return (np.array([round(math.ldexp(x, k2)) for x in t2], dtype=np.int64), k2,
+                np.array([round(math.ldexp(x, k3)) for x in t3], dtype=np.int64), k3)
+
     @property
     def E(self) -> int:
         return self.V * 5

@@ -43,11 +43,11 @@ constexpr int NO_TOP = CLV_MAX_EDGES;     // lat_by_rank[NO_TOP] == 0: nothing l
 enum { MODE_BEST_ALL = 0, MODE_UNIFORM_ALL = 1, MODE_UNIFORM_PROPOSAL = 2 };
 
 struct __align__(16) ARow {
-    double thr, acc, en, idle;
+    double thr, acc, en, idle, t2, t3;     // fixed-point rows as exact fp64 integers
 };
 
-struct __align__(8) RemEnt {            // one removal multiset R (single edge or pair), 64 B
-    double b0, b1, b2, b3;                 // centre aggregates minus the rows of R (exact integers)
+struct __align__(8) RemEnt {            // one removal multiset R (single edge or pair), 80 B
+    double b0, b1, b2, b3, b4, b5;         // centre aggregates minus the rows of R (exact integers)
     unsigned long long pm;                 // latency-rank presence mask after the removal
     int pre;                               // doubles: exclusive prefix of move-list lengths
     int end;                               // doubles: pre + move-list length
@@ -114,7 +114,7 @@ struct __align__(16) AnnealSmem {
     unsigned char pair_len[MAXP];
     // centre
     int w[CLV_MAX_EDGES];
-    double S[4];
+    double S[6];
     double mcount;                         // instances of the chain (every GED move keeps it)
     int svec[CLV_K];
     unsigned long long pmask;              // presence by latency rank
@@ -142,9 +142,8 @@ struct __align__(16) AnnealSmem {
 struct CandWalk {
     const AnnealSmem *s;
     unsigned long long pm;
-    double c20;
     int k1, k2, j1, j2;
-    __device__ __forceinline__ double operator()(double W0) const {
+    __device__ __forceinline__ double operator()(double W0, double c20) const {
         const AnnealSmem &S = *s;
         const int a = k1, b = k2, c = j1, d = j2;
         return p95_walk(pm, W0, c20, S.svc_by_rank, S.lat_by_rank, [&](int r) {
@@ -158,8 +157,7 @@ struct GraphWalk {
     const int *w;                          // weights by edge
     const unsigned char *edge_of_rank;
     unsigned long long pm;
-    double c20;
-    __device__ __forceinline__ double operator()(double W0) const {
+    __device__ __forceinline__ double operator()(double W0, double c20) const {
         const int *ww = w;
         const unsigned char *eo = edge_of_rank;
         return p95_walk(pm, W0, c20, s->svc_by_rank, s->lat_by_rank, [&](int r) { return (double)ww[eo[r]]; });
@@ -183,12 +181,13 @@ __device__ inline void decode_move(const AnnealSmem &s, int E, long long idx64, 
 
 // Full score of a move from the centre (decision path: proposal, log).
 __device__ inline Score score_move(const AnnealSmem &s, int r1, int r2, int a1, int a2) {
-    double t = s.S[0], ac = s.S[1], en = s.S[2], id = s.S[3];
+    double t = s.S[0], ac = s.S[1], en = s.S[2], id = s.S[3], q2 = s.S[4], q3 = s.S[5];
     unsigned long long m = s.pmask;
     const int e[2] = {r1, r2};
     for (int k = 0; k < 2; ++k) {
         if (e[k] == 0xFF) continue;
         t -= s.row[e[k]].thr; ac -= s.row[e[k]].acc; en -= s.row[e[k]].en; id -= s.row[e[k]].idle;
+        q2 -= s.row[e[k]].t2; q3 -= s.row[e[k]].t3;
     }
     if (r1 != 0xFF && s.w[r1] - 1 - (r2 == r1 ? 1 : 0) == 0) m &= ~s.rbit[r1];
     if (r2 != 0xFF && r2 != r1 && s.w[r2] - 1 == 0) m &= ~s.rbit[r2];
@@ -196,11 +195,12 @@ __device__ inline Score score_move(const AnnealSmem &s, int r1, int r2, int a1, 
     for (int k = 0; k < 2; ++k) {
         if (f[k] == 0xFF) continue;
         t += s.row[f[k]].thr; ac += s.row[f[k]].acc; en += s.row[f[k]].en; id += s.row[f[k]].idle;
+        q2 += s.row[f[k]].t2; q3 += s.row[f[k]].t3;
         m |= s.rbit[f[k]];
     }
-    CandWalk cw{&s, m, s.ec.c20, r1 == 0xFF ? 0xFF : s.rk[r1], r2 == 0xFF ? 0xFF : s.rk[r2],
+    CandWalk cw{&s, m, r1 == 0xFF ? 0xFF : s.rk[r1], r2 == 0xFF ? 0xFF : s.rk[r2],
                 a1 == 0xFF ? 0xFF : s.rk[a1], a2 == 0xFF ? 0xFF : s.rk[a2]};
-    return epilogue_d(t, ac, en, id, s.mcount, s.ec, cw);
+    return epilogue_d(t, ac, en, id, q2, q3, s.mcount, s.ec, cw);
 }
 
 // Apply a move to a bare weight vector (best-graph reconstruction).
@@ -221,7 +221,7 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
     decode_move(s, E, idx, r1, r2, a1, a2);
     const bool two = r2 != 0xFF;                   // a double move has r2 and a2
     const ARow R1 = s.row[r1], A1 = s.row[a1];
-    ARow R2 = {0.0, 0.0, 0.0, 0.0}, A2 = {0.0, 0.0, 0.0, 0.0};
+    ARow R2 = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, A2 = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     int wr2 = 0, wa2 = 0;
     if (two) { R2 = s.row[r2]; A2 = s.row[a2]; wr2 = s.w[r2]; wa2 = s.w[a2]; }
     const int wr1 = s.w[r1], wa1 = s.w[a1];
@@ -232,6 +232,8 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
     s.S[1] = s.S[1] + ((A1.acc + A2.acc) - (R1.acc + R2.acc));
     s.S[2] = s.S[2] + ((A1.en + A2.en) - (R1.en + R2.en));
     s.S[3] = s.S[3] + ((A1.idle + A2.idle) - (R1.idle + R2.idle));
+    s.S[4] = s.S[4] + ((A1.t2 + A2.t2) - (R1.t2 + R2.t2));
+    s.S[5] = s.S[5] + ((A1.t3 + A2.t3) - (R1.t3 + R2.t3));
     const int nr1 = wr1 - 1 - ((two && r2 == r1) ? 1 : 0);
     const int nr2 = two ? ((r2 == r1) ? nr1 : wr2 - 1) : 1;
     const int na1 = wa1 + 1 + ((two && a2 == a1) ? 1 : 0);
@@ -400,6 +402,8 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
         r.b1 = s.S[1] + -(s.row[x].acc + s.row[y].acc);
         r.b2 = s.S[2] + -(s.row[x].en + s.row[y].en);
         r.b3 = s.S[3] + -(s.row[x].idle + s.row[y].idle);
+        r.b4 = s.S[4] + -(s.row[x].t2 + s.row[y].t2);
+        r.b5 = s.S[5] + -(s.row[x].t3 + s.row[y].t3);
         unsigned long long m = s.pmask;
         if (x == y) { if (s.w[x] == 2) m &= ~s.rbit[x]; }
         else {
@@ -422,6 +426,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             RemEnt &r = s.se[i];
             r.b0 = s.S[0] + -s.row[e].thr; r.b1 = s.S[1] + -s.row[e].acc;
             r.b2 = s.S[2] + -s.row[e].en; r.b3 = s.S[3] + -s.row[e].idle;
+            r.b4 = s.S[4] + -s.row[e].t2; r.b5 = s.S[5] + -s.row[e].t3;
             r.pm = (s.w[e] == 1) ? (s.pmask & ~s.rbit[e]) : s.pmask;
             r.k1 = s.rk[e]; r.k2 = 0xFF;
             r.ibase = e * E;
@@ -450,8 +455,8 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
 // scenarios, IEEE division (a scenario outside fast_div_safe's ranges).
 template <int MODE, int EC>
 __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args, double t, double ac, double en,
-                                     double id, const CandWalk &cw, double mcnt, int idx, KRec &rS, KRec &rV,
-                                     KRec &rP, uint64_t seed, uint64_t gchain, uint64_t k) {
+                                     double id, double q2, double q3, const CandWalk &cw, double mcnt, int idx,
+                                     KRec &rS, KRec &rV, KRec &rP, uint64_t seed, uint64_t gchain, uint64_t k) {
     if (MODE == MODE_UNIFORM_PROPOSAL) {
         const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
         if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; }
@@ -460,8 +465,8 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args
     // one evaluation scenario for every chain: its constants are kernel parameters
     // (constant-bank operands); per-chain scenarios come from the CTA's shared copy
     Score sc;
-    if constexpr (EC == 2) sc = epilogue_t<true>(t, ac, en, id, mcnt, args.ec0, cw);
-    else sc = epilogue_t<EC == 1>(t, ac, en, id, mcnt, s.ec, cw);
+    if constexpr (EC == 2) sc = epilogue_t<true>(t, ac, en, id, q2, q3, mcnt, args.ec0, cw);
+    else sc = epilogue_t<EC == 1>(t, ac, en, id, q2, q3, mcnt, s.ec, cw);
     const unsigned long long key = okey(sc.h);
     if (sc.sla) { if (krec_less(key, idx, rS)) { rS.key = key; rS.idx = idx; } }
     else        { if (krec_less(key, idx, rV)) { rV.key = key; rV.idx = idx; } }
@@ -505,6 +510,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         s.row[e].acc = (double)T.acc_q[e];
         s.row[e].en = (double)T.en_q[e];
         s.row[e].idle = (double)T.idle_q[e % 5];
+        s.row[e].t2 = (double)T.t2_q[e];
+        s.row[e].t3 = (double)T.t3_q[e];
         s.lat_by_rank[e] = T.lat_by_rank[e];
         s.svc_by_rank[e] = T.svc_by_rank[e];
         s.rbit[e] = 1ULL << T.rank[e];
@@ -525,17 +532,18 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     __syncthreads();
     if (tid == 0) {
         const uint16_t *w0 = args.start_w + (size_t)chain * E;
-        double S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+        double S0 = 0, S1 = 0, S2 = 0, S3 = 0, S4 = 0, S5 = 0;
         unsigned long long m = 0;
         for (int k = 0; k < CLV_K; ++k) { s.svec[k] = 0; s.fsvec[k] = -1; }
         for (int e = 0; e < E; ++e) {
             const int x = w0[e];
             s.w[e] = x;
             S0 += x * s.row[e].thr; S1 += x * s.row[e].acc; S2 += x * s.row[e].en; S3 += x * s.row[e].idle;
+            S4 += x * s.row[e].t2; S5 += x * s.row[e].t3;
             s.svec[e % 5] += x;
             if (x > 0) m |= s.rbit[e];
         }
-        s.S[0] = S0; s.S[1] = S1; s.S[2] = S2; s.S[3] = S3;
+        s.S[0] = S0; s.S[1] = S1; s.S[2] = S2; s.S[3] = S3; s.S[4] = S4; s.S[5] = S5;
         s.pmask = m;
         int cnt = 0;
         for (int e = 0; e < E; ++e) { cnt += s.w[e]; s.wr[s.rk[e]] = (double)s.w[e]; }
@@ -559,8 +567,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         }
         if (tot < 1 || !feasible(args.F, n, s.svec[0], s.svec[1], s.svec[2], s.svec[3], s.svec[4])) invalid = 1;
         edge_evals = __popcll(s.pmask);
-        const Score sc = epilogue_d(s.S[0], s.S[1], s.S[2], s.S[3], s.mcount, s.ec,
-                                    GraphWalk{&s, s.w, s.er, s.pmask, s.ec.c20});
+        const Score sc = epilogue_d(s.S[0], s.S[1], s.S[2], s.S[3], s.S[4], s.S[5], s.mcount, s.ec,
+                                    GraphWalk{&s, s.w, s.er, s.pmask});
         hc = sc.h;
         bk1 = sc.sla ? 0u : 1u; bk2 = okey(sc.h);
         for (int e = 0; e < E; ++e) s.bw[e] = s.w[e];
@@ -573,7 +581,6 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     const int G = CL * ANT;
     const int gt = crank * ANT + tid;
     const unsigned long long mem_ok = s.mem_ok;
-    const double c20 = EC == 2 ? args.ec0.c20 : s.ec.c20;
 
     for (int k = 0; !done; ++k) {
         PROF_MARK(0);
@@ -598,9 +605,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (a != R.r1 && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]]) {
                     ++cnt;
                     const ARow &A = s.row[a];
-                    const CandWalk cw{&s, R.pm | s.rbit[a], c20, R.k1, 0xFF, s.rk[a], 0xFF};
+                    const CandWalk cw{&s, R.pm | s.rbit[a], R.k1, 0xFF, s.rk[a], 0xFF};
                     fold<MODE, EC>(s, args, R.b0 + A.thr, R.b1 + A.acc, R.b2 + A.en,
-                               R.b3 + A.idle, cw, mcnt, R.ibase + a,
+                               R.b3 + A.idle, R.b4 + A.t2, R.b5 + A.t3, cw, mcnt, R.ibase + a,
                                rS, rV, rP, args.seed, gchain, (uint64_t)k);
                 }
                 i += dI; a += dA;
@@ -637,10 +644,11 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                                 ++cnt;
                                 const int a1 = ent & 63, a2 = (ent >> 6) & 63;
                                 const ARow &A1 = s.row[a1], &A2 = s.row[a2];
-                                const CandWalk cw{&s, R.pm | s.rbit[a1] | s.rbit[a2], c20, R.k1, R.k2,
+                                const CandWalk cw{&s, R.pm | s.rbit[a1] | s.rbit[a2], R.k1, R.k2,
                                                   s.rk[a1], s.rk[a2]};
                                 fold<MODE, EC>(s, args, R.b0 + A1.thr + A2.thr, R.b1 + A1.acc + A2.acc,
-                                           R.b2 + A1.en + A2.en, R.b3 + A1.idle + A2.idle, cw, mcnt,
+                                           R.b2 + A1.en + A2.en, R.b3 + A1.idle + A2.idle,
+                                           R.b4 + A1.t2 + A2.t2, R.b5 + A1.t3 + A2.t3, cw, mcnt,
                                            R.ibase + (int)(ent >> 17), rS, rV, rP, args.seed,
                                            gchain, (uint64_t)k);
                             }
@@ -784,16 +792,17 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         clv_chain_result r;
         uint16_t *bw_out = args.best_w + (size_t)chain * E;
         uint16_t *fw_out = args.final_w + (size_t)chain * E;
-        double S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+        double S0 = 0, S1 = 0, S2 = 0, S3 = 0, S4 = 0, S5 = 0;
         unsigned long long m = 0;
         for (int e = 0; e < E; ++e) {
             const int x = s.bw[e];
             bw_out[e] = (uint16_t)x;
             fw_out[e] = (uint16_t)s.w[e];
             S0 += x * s.row[e].thr; S1 += x * s.row[e].acc; S2 += x * s.row[e].en; S3 += x * s.row[e].idle;
+            S4 += x * s.row[e].t2; S5 += x * s.row[e].t3;
             if (x > 0) m |= s.rbit[e];
         }
-        const Score sb = epilogue_d(S0, S1, S2, S3, s.mcount, s.ec, GraphWalk{&s, s.bw, s.er, m, s.ec.c20});   // moves keep m
+        const Score sb = epilogue_d(S0, S1, S2, S3, S4, S5, s.mcount, s.ec, GraphWalk{&s, s.bw, s.er, m});   // moves keep m
         r.f = sb.f; r.h = sb.h; r.p95_ms = sb.L; r.accuracy = sb.A; r.energy_wh = sb.E;
         r.sla_met = sb.sla;
         r.status = status; r.steps = steps; r.best_step = best_step;
@@ -878,6 +887,8 @@ cudaError_t launch_anneal(const AnnealArgs &a, int cluster_size, cudaStream_t st
             case 2: return launch_mode<MODE_BEST_ALL, 4, 1>(a, cluster_size, st);
             case 3: return launch_mode<MODE_BEST_ALL, 3, 3>(a, cluster_size, st);
             case 4: return launch_mode<MODE_BEST_ALL, 3, 4>(a, cluster_size, st);
+            case 5: return launch_mode<MODE_BEST_ALL, 2, 2>(a, cluster_size, st);
+            case 6: return launch_mode<MODE_BEST_ALL, 2, 4>(a, cluster_size, st);
             case 9: return launch_mode<MODE_BEST_ALL, 3, 2, true>(a, cluster_size, st);
             default: return launch_mode<MODE_BEST_ALL, 3, 2>(a, cluster_size, st);
         }

@@ -48,8 +48,12 @@ int make_ec(clv_ctx *ctx, const clv_eval_params *p, const FamilyTables &T, EvalC
     double R = p->arrival_rps;
     ec.R_q = std::ldexp(R, T.kt);
     ec.inv_3600R = 1.0 / (3600.0 * R);
-    ec.kW = 1000.0 / R;
+    ec.R = R;
+    ec.iR = 1.0 / R;
     ec.c20 = 20000.0 / R;
+    ec.sc1 = std::ldexp(1.0, -T.kt);
+    ec.sc2 = std::ldexp(1.0, -T.k2);
+    ec.sc3 = std::ldexp(1.0, -T.k3);
     ec.en_scale = std::ldexp(1.0, T.kt - T.ke);
     ec.idle_scale = std::ldexp(1.0, -T.ki);
     ec.rho_sat = p->rho_sat;
@@ -256,6 +260,24 @@ int clv_set_profile(clv_ctx *ctx, int family, int V, const int64_t *thr_q, const
         if (idle_q5[k] < 0 || idle_q5[k] >= LIM) return fail(ctx, CLV_ERR_PROFILE, "idle row out of range");
         T.idle_q[k] = idle_q5[k];
     }
+    {   // rate moments thr^2, thr^3 (thr = 1000 / svc) as fixed-point rows < 2^31 (round half even,
+        // as oracle/tables.py::rate_moment_rows)
+        double t2[CLV_MAX_EDGES], t3[CLV_MAX_EDGES], m2 = 0.0, m3 = 0.0;
+        for (int e = 0; e < T.E; ++e) {
+            const double thr = 1000.0 / svc_ms[e];
+            t2[e] = thr * thr;
+            t3[e] = t2[e] * thr;
+            m2 = std::max(m2, t2[e]);
+            m3 = std::max(m3, t3[e]);
+        }
+        int ex;
+        std::frexp(m2, &ex); T.k2 = 31 - ex;
+        std::frexp(m3, &ex); T.k3 = 31 - ex;
+        for (int e = 0; e < T.E; ++e) {
+            T.t2_q[e] = (long long)std::nearbyint(std::ldexp(t2[e], T.k2));
+            T.t3_q[e] = (long long)std::nearbyint(std::ldexp(t3[e], T.k3));
+        }
+    }
     std::vector<int> ord(T.E);
     for (int e = 0; e < T.E; ++e) ord[e] = e;
     std::sort(ord.begin(), ord.end(), [&](int x, int y) {
@@ -419,7 +441,7 @@ int clv_score_graphs(clv_ctx *ctx, int family, const uint16_t *w_dev, int64_t co
     a.count = count; a.index_base = index_base; a.w = w_dev; a.topo = ctx->topo_dev;
     a.f_out = f_dev; a.h_out = h_dev; a.p95_out = p95_dev; a.sla_out = sla_dev; a.feas_out = feas_dev;
     a.sel = make_sel(ctx);
-    a.fast = fast_div_safe(a.ec, ctx->fam[family].lat95, ctx->fam[family].E) ? 1 : 0;
+    a.fast = fast_div_safe(a.ec, ctx->fam[family].lat95, ctx->fam[family].svc, ctx->fam[family].E) ? 1 : 0;
     CLV_CUDA(launch_score_graphs(a, ctx->fam[family], grid_for(ctx, count, 256), st), "score_graphs");
     if (!best) return CLV_OK;
     return fetch_best(ctx, select_mode, st, best);
@@ -442,7 +464,7 @@ int clv_score_x(clv_ctx *ctx, int family, int n, const uint8_t *xp_dev, const ui
     a.xp = xp_dev; a.xv = xv_dev; a.xv_off = xv_off_dev; a.topo = ctx->topo_dev;
     a.f_out = f_dev; a.h_out = h_dev; a.sla_out = sla_dev; a.sel = make_sel(ctx);
     a.error_key = reinterpret_cast<unsigned long long *>(ctx->err_index);
-    a.fast = fast_div_safe(a.ec, ctx->fam[family].lat95, ctx->fam[family].E) ? 1 : 0;
+    a.fast = fast_div_safe(a.ec, ctx->fam[family].lat95, ctx->fam[family].svc, ctx->fam[family].E) ? 1 : 0;
     CLV_CUDA(launch_score_x(a, n, grid_for(ctx, count, 256), st), "score_x");
     CLV_CUDA(cudaMemcpyAsync(ctx->host_err + 2, ctx->err_index, sizeof(long long), cudaMemcpyDeviceToHost, st), "copy err key");
     rc = fetch_best(ctx, select_mode, st, best);
@@ -528,7 +550,7 @@ int clv_oracle_search(clv_ctx *ctx, int family, int n, int64_t begin, int64_t en
     CLV_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
     a.fam = ctx->fam_dev + family; a.topo = ctx->topo_dev; a.begin = begin; a.end = end; a.n = n;
     a.sel = make_sel(ctx);
-    a.fast = fast_div_safe(a.ec, ctx->fam[family].lat95, ctx->fam[family].E) ? 1 : 0;
+    a.fast = fast_div_safe(a.ec, ctx->fam[family].lat95, ctx->fam[family].svc, ctx->fam[family].E) ? 1 : 0;
     CLV_CUDA(launch_oracle(a, grid_for(ctx, end - begin, 256), st), "oracle");
     return fetch_best(ctx, CLV_SELECT_ORACLE, st, best);
 }
@@ -570,7 +592,7 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
     a.fam = ctx->fam_dev + family; a.F = feas_view(ctx); a.ec = ctx->ec_dev; a.n_ec = n_params; a.ec0 = ecs[0];
     a.fast_div = 1;
     for (int i = 0; i < n_params; ++i)
-        if (!fast_div_safe(ecs[i], ctx->fam[family].lat95, ctx->fam[family].E)) a.fast_div = 0;
+        if (!fast_div_safe(ecs[i], ctx->fam[family].lat95, ctx->fam[family].svc, ctx->fam[family].E)) a.fast_div = 0;
     a.t_init = ap->t_init; a.cooling = ap->cooling_step; a.t_floor = ap->t_floor;
     a.stall_limit = ap->stall_limit; a.max_steps = ap->max_steps; a.proposal = ap->proposal; a.evaluate = ap->evaluate;
     a.n = n; a.n_chains = n_chains; a.E = ctx->fam[family].E; a.chain_base = chain_base; a.seed = seed;
@@ -697,7 +719,7 @@ int clv_sweep(clv_ctx *ctx, int n_pods, const clv_pod *pods, int64_t begin, int6
     a.fast = 1;
     for (int p = 0; p < a.n_pods; ++p) {
         const FamilyTables &T = ctx->fam[a.pods[p].family];
-        if (!fast_div_safe(a.pods[p].ec, T.lat95, T.E)) a.fast = 0;
+        if (!fast_div_safe(a.pods[p].ec, T.lat95, T.svc, T.E)) a.fast = 0;
     }
     CLV_CUDA(launch_sweep(a, grid_for(ctx, end - begin, 256), st), "sweep");
     if (!best) return CLV_OK;

@@ -17,7 +17,7 @@ namespace clv {
 constexpr int SNT = 256;
 
 struct __align__(16) ERow {
-    long long thr, acc, en, idle;
+    long long thr, acc, en, idle, t2, t3;
 };
 
 struct RankTabs {                             // per-family latency-rank tables (shared memory)
@@ -42,6 +42,8 @@ __device__ inline void stage_rows(ERow *row, RankTabs &rt, const FamilyTables &T
         row[e].acc = T.acc_q[e];
         row[e].en = T.en_q[e];
         row[e].idle = T.idle_q[e % 5];
+        row[e].t2 = T.t2_q[e];
+        row[e].t3 = T.t3_q[e];
     }
     stage_ranks(rt, T);
 }
@@ -52,8 +54,7 @@ struct EdgeWalk {
     const RankTabs *rt;
     const W *w;
     unsigned long long pm;                     // presence by latency rank
-    double c20;
-    __device__ __forceinline__ double operator()(double W0) const {
+    __device__ __forceinline__ double operator()(double W0, double c20) const {
         const RankTabs &t = *rt;
         const W *ww = w;
         return p95_walk(pm, W0, c20, t.svc, t.lat, [&](int r) { return (double)ww[t.edge[r]]; });
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(SNT) score_graphs_kernel(const __grid_constant
         __syncthreads();
         if (threadIdx.x < rows) {
             const uint16_t *w = tile + threadIdx.x * E;
-            long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+            long long S0 = 0, S1 = 0, S2 = 0, S3 = 0, S4 = 0, S5 = 0;
             int sv[CLV_K] = {0, 0, 0, 0, 0};
             unsigned long long m = 0;
             bool memfail = false;
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(SNT) score_graphs_kernel(const __grid_constant
                 const long long x = w[e];
                 if (x) {
                     S0 += x * row[e].thr; S1 += x * row[e].acc; S2 += x * row[e].en; S3 += x * row[e].idle;
+                    S4 += x * row[e].t2; S5 += x * row[e].t3;
                     sv[e % 5] += (int)x;
                     m |= 1ULL << rt.rank[e];
                     memfail |= !((mem_ok >> e) & 1ULL);
@@ -125,9 +127,9 @@ __global__ void __launch_bounds__(SNT) score_graphs_kernel(const __grid_constant
             const long long i = base + threadIdx.x;
             const bool feas = !memfail && m != 0 && feasible(a.F, n, sv[0], sv[1], sv[2], sv[3], sv[4]);
             if (feas) {
-                Score sc = epilogue_d((double)S0, (double)S1, (double)S2, (double)S3,
+                Score sc = epilogue_d((double)S0, (double)S1, (double)S2, (double)S3, (double)S4, (double)S5,
                                       (double)(sv[0] + sv[1] + sv[2] + sv[3] + sv[4]), a.ec,
-                                      EdgeWalk<uint16_t>{&rt, w, m, a.ec.c20});
+                                      EdgeWalk<uint16_t>{&rt, w, m});
                 ++c_valid;
                 c_sla += sc.sla;
                 consider(r0, r1, sc, a.index_base + i, a.select_mode);
@@ -184,7 +186,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
 // Per-family rows as kernel parameters (constant bank): with the edge loop fully
 // unrolled (template on V) every row value is a compile-time constant-bank operand.
 struct GraphRows {
-    double thr[CLV_MAX_EDGES], acc[CLV_MAX_EDGES], en[CLV_MAX_EDGES];
+    double thr[CLV_MAX_EDGES], acc[CLV_MAX_EDGES], en[CLV_MAX_EDGES], t2[CLV_MAX_EDGES], t3[CLV_MAX_EDGES];
     double idle[CLV_K];
     unsigned long long bad;                 // bit rank(e): edge e is memory-infeasible
     unsigned char rk[CLV_MAX_EDGES];        // latency rank of edge e
@@ -238,12 +240,12 @@ __global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_cons
                 __syncthreads();
             }
         }
-        double S0[CPT], S1[CPT], S2[CPT];
+        double S0[CPT], S1[CPT], S2[CPT], S4[CPT], S5[CPT];
         int sv[CPT][CLV_K];
         unsigned long long pe[CPT];
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
-            S0[c] = S1[c] = S2[c] = 0.0;
+            S0[c] = S1[c] = S2[c] = S4[c] = S5[c] = 0.0;
             pe[c] = 0ULL;
 #pragma unroll
             for (int k = 0; k < CLV_K; ++k) sv[c][k] = 0;
@@ -258,6 +260,8 @@ __global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_cons
                 S0[c] = __fma_rn(xd, R.thr[e], S0[c]);
                 S1[c] = __fma_rn(xd, R.acc[e], S1[c]);
                 S2[c] = __fma_rn(xd, R.en[e], S2[c]);
+                S4[c] = __fma_rn(xd, R.t2[e], S4[c]);
+                S5[c] = __fma_rn(xd, R.t3[e], S5[c]);
                 sv[c][e % CLV_K] += x;
                 pe[c] |= (unsigned long long)(x != 0) << R.rk[e];
             }
@@ -273,9 +277,9 @@ __global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_cons
             const bool feas = !(pe[c] & R.bad) && pe[c] != 0 &&
                               feasible(a.F, n, sv[c][0], sv[c][1], sv[c][2], sv[c][3], sv[c][4]);
             if (feas) {
-                Score sc = epilogue_t<FAST>(S0[c], S1[c], S2[c], S3,
+                Score sc = epilogue_t<FAST>(S0[c], S1[c], S2[c], S3, S4[c], S5[c],
                                             (double)(sv[c][0] + sv[c][1] + sv[c][2] + sv[c][3] + sv[c][4]), a.ec,
-                                            EdgeWalk<uint16_t>{&rt, w0 + c * SNT * E, pe[c], a.ec.c20});
+                                            EdgeWalk<uint16_t>{&rt, w0 + c * SNT * E, pe[c]});
                 ++c_valid;
                 c_sla += sc.sla;
                 consider(r0, r1, sc, a.index_base + i, a.select_mode);
@@ -319,6 +323,7 @@ cudaError_t launch_score_graphs(const ScoreArgs &a, const FamilyTables &T, int g
         GraphRows R{};
         for (int e = 0; e < T.E; ++e) {
             R.thr[e] = (double)T.thr_q[e]; R.acc[e] = (double)T.acc_q[e]; R.en[e] = (double)T.en_q[e];
+            R.t2[e] = (double)T.t2_q[e]; R.t3[e] = (double)T.t3_q[e];
             R.rk[e] = T.rank[e];
             if (!((T.mem_ok >> e) & 1ULL)) R.bad |= 1ULL << T.rank[e];
         }
@@ -367,9 +372,10 @@ constexpr int X_SMEM = 40 * 1024;           // dynamic staging bytes: x^p tile, 
 
 template <bool XP_SMEM, bool XV_SMEM, bool HIST>
 __device__ __forceinline__ void walk_row(unsigned short *hc, const uint8_t *xpr, const uint8_t *xvr, int mcnt, int n,
-                                         int V, const unsigned *cfg, const int4 *row, const unsigned char *rank_ok,
-                                         long long &S0, long long &S1, long long &S2, long long &S3,
-                                         unsigned long long &m, int &err) {
+                                         int V, const unsigned *cfg, const int4 *row, const int2 *row2,
+                                         const unsigned char *rank_ok, long long &S0, long long &S1, long long &S2,
+                                         long long &S3, long long &S4, long long &S5, unsigned long long &m,
+                                         int &err) {
     // cfg[id]: bit 31 valid, bits 24..27 slice count (1..7), bits 0..20 slice kinds (3 bits each).
     // HIST: slot counts per bucket b = min(v, V + 1) * 5 + kind -- bucket row 0 holds the
     // variants < 1, rows 1..V the edges (v - 1) * 5 + kind, row V + 1 the variants > V --
@@ -396,9 +402,10 @@ __device__ __forceinline__ void walk_row(unsigned short *hc, const uint8_t *xpr,
             const bool vok = (unsigned)(v - 1) < (unsigned)V;
             const int e = vok ? (v - 1) * 5 + kind : 0;
             const int4 R = row[e];
+            const int2 R2 = row2[e];
             const unsigned ro = rank_ok[e];
             infeas |= !vok || !ro;
-            S0 += R.x; S1 += R.y; S2 += R.z; S3 += R.w;
+            S0 += R.x; S1 += R.y; S2 += R.z; S3 += R.w; S4 += R2.x; S5 += R2.y;
             m |= 1ULL << (ro & 63);
         }
     }
@@ -409,8 +416,10 @@ __device__ __forceinline__ void walk_row(unsigned short *hc, const uint8_t *xpr,
             if (b < 5) { lt1 |= c != 0; continue; }
             if (b >= 5 * (V + 1)) { infeas |= c != 0; continue; }
             const int4 R = row[b - 5];
+            const int2 R2 = row2[b - 5];
             const unsigned ro = rank_ok[b - 5];
             S0 += (long long)c * R.x; S1 += (long long)c * R.y; S2 += (long long)c * R.z; S3 += (long long)c * R.w;
+            S4 += (long long)c * R2.x; S5 += (long long)c * R2.y;
             if (c) { m |= 1ULL << (ro & 63); infeas |= !ro; }
         }
     }
@@ -451,6 +460,7 @@ template <bool FAST>
 __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ ScoreArgs a, int n, int xp_stride,
                                                      int xv_cap) {
     __shared__ int4 row[CLV_MAX_EDGES];
+    __shared__ int2 row2[CLV_MAX_EDGES];               // rate-moment rows t2_q, t3_q
     __shared__ RankTabs rt;
     __shared__ unsigned char rank_ok[CLV_MAX_EDGES];   // 0x40 | rank when memory-feasible, else 0
     __shared__ unsigned cfg[256];
@@ -464,6 +474,7 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
         const bool live = e < T.E;
         row[e] = live ? make_int4((int)T.thr_q[e], (int)T.acc_q[e], (int)T.en_q[e], (int)T.idle_q[e % 5])
                       : make_int4(0, 0, 0, 0);
+        row2[e] = live ? make_int2((int)T.t2_q[e], (int)T.t3_q[e]) : make_int2(0, 0);
         rank_ok[e] = (live && ((T.mem_ok >> e) & 1ULL)) ? (unsigned char)(0x40 | T.rank[e]) : 0;
     }
     stage_ranks(rt, T);
@@ -519,7 +530,7 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
         if (threadIdx.x < rows) {
             const long long c = c0 + threadIdx.x;
             const long long o0 = __ldg(a.xv_off + c), o1 = __ldg(a.xv_off + c + 1);
-            long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+            long long S0 = 0, S1 = 0, S2 = 0, S3 = 0, S4 = 0, S5 = 0;
             unsigned long long m = 0;
             int err;
             unsigned short *hc = hist + threadIdx.x;
@@ -532,22 +543,22 @@ __global__ void __launch_bounds__(XT) score_x_kernel(const __grid_constant__ Sco
                 const uint8_t *sxr = sxv + lead + (o0 - G0);
                 const uint8_t *sxpr = sxp + threadIdx.x * xp_stride;
                 if (mcnt > 0xFFFF)
-                    walk_row<false, false, false>(hc, gxpr, gxr, mcnt, n, V, cfg, row, rank_ok, S0, S1, S2, S3, m, err);
+                    walk_row<false, false, false>(hc, gxpr, gxr, mcnt, n, V, cfg, row, row2, rank_ok, S0, S1, S2, S3, S4, S5, m, err);
                 else if (xp_stride && xv_fits)
-                    walk_row<true, true, true>(hc, sxpr, sxr, mcnt, n, V, cfg, row, rank_ok, S0, S1, S2, S3, m, err);
+                    walk_row<true, true, true>(hc, sxpr, sxr, mcnt, n, V, cfg, row, row2, rank_ok, S0, S1, S2, S3, S4, S5, m, err);
                 else if (xp_stride)
-                    walk_row<true, false, true>(hc, sxpr, gxr, mcnt, n, V, cfg, row, rank_ok, S0, S1, S2, S3, m, err);
+                    walk_row<true, false, true>(hc, sxpr, gxr, mcnt, n, V, cfg, row, row2, rank_ok, S0, S1, S2, S3, S4, S5, m, err);
                 else
-                    walk_row<false, false, true>(hc, gxpr, gxr, mcnt, n, V, cfg, row, rank_ok, S0, S1, S2, S3, m, err);
+                    walk_row<false, false, true>(hc, gxpr, gxr, mcnt, n, V, cfg, row, row2, rank_ok, S0, S1, S2, S3, S4, S5, m, err);
             }
             if (err) {
                 atomicMin(a.error_key, ((unsigned long long)c << 8) | (unsigned)err);
                 if (a.sla_out) a.sla_out[c] = 0;
             } else {
                 const int mc = (int)(o1 - o0);
-                Score sc = epilogue_t<FAST>((double)S0, (double)S1, (double)S2, (double)S3, (double)mc, a.ec,
-                                            [&](double W0) {
-                    return p95_walk(m, W0, a.ec.c20, rt.svc, rt.lat, [&](int r) {
+                Score sc = epilogue_t<FAST>((double)S0, (double)S1, (double)S2, (double)S3, (double)S4, (double)S5,
+                                            (double)mc, a.ec, [&](double W0, double c20) {
+                    return p95_walk(m, W0, c20, rt.svc, rt.lat, [&](int r) {
                         const int e = rt.edge[r];
                         return (double)(long_row ? count_edge_slots(gxpr, gxr, mc, n, cfg, e) : hc[(e + 5) * XT]);
                     });
@@ -606,7 +617,7 @@ __global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ Ora
         while (r + 1 < P.K && a.row_off[r + 1] <= i) ++r;
         // within a row the index is < 8^7 (variants per slice ^ slices): 32-bit digits
         unsigned rem = (unsigned)(i - a.row_off[r]);
-        long long S0 = 0, S1 = 0, S2 = 0, S3 = 0;
+        long long S0 = 0, S1 = 0, S2 = 0, S3 = 0, S4 = 0, S5 = 0;
         unsigned long long m = 0;
         const int ns = P.nslices[r];
         unsigned long long rks = 0;                // latency rank of slice j in byte j
@@ -617,13 +628,15 @@ __global__ void __launch_bounds__(SNT) oracle_kernel(const __grid_constant__ Ora
             const int k = P.kinds[r][j];
             const int e = flist[k][dgt] * 5 + k;
             S0 += row[e].thr; S1 += row[e].acc; S2 += row[e].en; S3 += row[e].idle;
+            S4 += row[e].t2; S5 += row[e].t3;
             m |= 1ULL << rt.rank[e];
             rks |= (unsigned long long)rt.rank[e] << (8 * j);
         }
         const double nd = (double)n;
         Score sc = epilogue_t<FAST>((double)(S0 * n), (double)(S1 * n), (double)(S2 * n), (double)(S3 * n),
-                                    (double)(n * ns), a.ec, [&](double W0) {
-            return p95_walk(m, W0, a.ec.c20, rt.svc, rt.lat, [&](int rr) {
+                                    (double)(S4 * n), (double)(S5 * n), (double)(n * ns), a.ec,
+                                    [&](double W0, double c20) {
+            return p95_walk(m, W0, c20, rt.svc, rt.lat, [&](int rr) {
                 int c = 0;
                 for (int j = 0; j < ns; ++j) c += (int)((rks >> (8 * j)) & 0xFF) == rr;
                 return (double)c * nd;             // exact: the standardized graph is n x the row
@@ -667,8 +680,8 @@ struct Draws {
     }
 };
 
-struct __align__(32) SRow {
-    double thr, acc, en, idle;
+struct __align__(16) SRow {
+    double thr, acc, en, idle, t2, t3;
 };
 
 constexpr int ZROW = CLV_MAX_EDGES;           // all-zero row: a configuration draw adds nothing
@@ -699,6 +712,8 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
             row[p][e].acc = real ? (double)T.acc_q[e] : 0.0;
             row[p][e].en = real ? (double)T.en_q[e] : 0.0;
             row[p][e].idle = real ? (double)T.idle_q[e % 5] : 0.0;
+            row[p][e].t2 = real ? (double)T.t2_q[e] : 0.0;
+            row[p][e].t3 = real ? (double)T.t3_q[e] : 0.0;
             rbit[p][e] = real ? (1ULL << T.rank[e]) : 0ULL;
         }
         stage_ranks(rt[p], T);
@@ -732,7 +747,7 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
         bool sla = true;
         for (int p = 0; p < a.n_pods; ++p) {
             // fp64 sums of exact integers (< 2^53): identical to the oracle's int64 sums
-            double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
+            double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0, S4 = 0.0, S5 = 0.0;
             unsigned long long m = 0;
             // One draw per iteration, in the oracle's order (oracle/search.py::draw_candidate):
             // a configuration draw when the current GPU's slices are exhausted, else the next
@@ -766,6 +781,7 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
                     const SRow &q = row[p][e];
                     S0 = __fma_rn(cd, q.thr, S0); S1 = __fma_rn(cd, q.acc, S1);
                     S2 = __fma_rn(cd, q.en, S2); S3 = __fma_rn(cd, q.idle, S3);
+                    S4 = __fma_rn(cd, q.t2, S4); S5 = __fma_rn(cd, q.t3, S5);
                     m |= c ? rbit[p][e] : 0ULL;
                 }
             } else {
@@ -776,7 +792,7 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
                     const int v = flist[p][k][(int)(((uint64_t)w * nfeas[p][k]) >> 32)];
                     const int e = cfg ? ZROW : v * 5 + k;
                     const SRow &q = row[p][e];
-                    S0 += q.thr; S1 += q.acc; S2 += q.en; S3 += q.idle;
+                    S0 += q.thr; S1 += q.acc; S2 += q.en; S3 += q.idle; S4 += q.t2; S5 += q.t3;
                     m |= rbit[p][e];
                     const int rn = (int)(((uint64_t)w * K) >> 32);
                     r = cfg ? rn : r;
@@ -788,8 +804,9 @@ __global__ void __launch_bounds__(SNT) sweep_kernel(const __grid_constant__ Swee
             }
             // the p95 walk reads the visited edges' counts (HIST), or recounts them by
             // replaying the pod's draws (pods with 7 n >= 2^16)
-            Score sc = epilogue_t<FAST>(S0, S1, S2, S3, (double)inst, a.pods[p].ec, [&](double W0) {
-                return p95_walk(m, W0, a.pods[p].ec.c20, rt[p].svc, rt[p].lat, [&](int rr) {
+            Score sc = epilogue_t<FAST>(S0, S1, S2, S3, S4, S5, (double)inst, a.pods[p].ec,
+                                        [&](double W0, double c20) {
+                return p95_walk(m, W0, c20, rt[p].svc, rt[p].lat, [&](int rr) {
                     const int e0 = rt[p].edge[rr];
                     if (HIST) return (double)hc[e0 * SNT];
                     Draws dd = d0;

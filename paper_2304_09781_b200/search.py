@@ -292,3 +292,36 @@ def random_fleets(engine: CloverEngine, profile: ProfileTable, n: int, seed: int
     probe = Scenario(n, 1.0, 0.0, ObjectiveParams(1.0, 1.0, 1.0, 0.5))
     pods = [(profile, probe, n, 1.0)]
     return [engine.sweep_decode(pods, seed, first + i)[0] for i in range(count)]
+
+
+def perturbed_fleets(incumbent: FleetConfig, profile: ProfileTable, seed: int, count: int, first: int = 0,
+                     keep: float = 0.75) -> list[FleetConfig]:
+    """Re-plan start points around a deployed fleet (a re-plan starts from the
+    incumbent): fleet i keeps each GPU's partition and variants with probability ``keep``
+    and otherwise redraws them as BLOVER does (uniform config id, uniform memory-feasible
+    variant per slice).  Draws come from derive_seed(seed, i, gpu, j) (core.py:104-118),
+    so the starts are reproducible on any host."""
+    topo = profile.topology
+    ids = list(topo.config_ids)
+    feas = {s: profile.feasible_variants(s) for s in SliceType}
+    inc_parts = list(incumbent.partitions)
+    inc_assign = list(incumbent.assignments)
+    starts = [0]
+    for cid in inc_parts:
+        starts.append(starts[-1] + len(topo.config_slices(cid)))
+    thresh = int(keep * (1 << 20))
+    out = []
+    for i in range(first, first + count):
+        parts, assign = [], []
+        for g, cid in enumerate(inc_parts):
+            if (derive_seed(seed, i, g, 0) & ((1 << 20) - 1)) < thresh:
+                parts.append(cid)
+                assign.extend(inc_assign[starts[g]:starts[g + 1]])
+                continue
+            c = ids[derive_seed(seed, i, g, 1) % len(ids)]
+            parts.append(c)
+            for j, s in enumerate(topo.config_slices(c)):
+                lst = feas[s]
+                assign.append(lst[derive_seed(seed, i, g, 2 + j) % len(lst)])
+        out.append(FleetConfig(parts, assign, topo))
+    return out

@@ -124,7 +124,7 @@ def test_reference_style_ctypes_binding_replans(engine):
         ap_py = bench.anneal_params(20)
         ap = AnnealParams(ap_py.t_init, ap_py.cooling_step, ap_py.t_floor, ap_py.stall_limit, ap_py.step_limit(),
                           0, 0)
-        starts = bench.make_starts(engine, prof, 3, 0, 24)
+        starts = bench.make_starts(prof, 3, 0, 24, 0.75)
         m, E = starts.shape
         w = (ctypes.c_uint16 * (m * E))(*[int(x) for x in starts.reshape(-1)])
         res, rec = (ChainResult * m)(), Record()

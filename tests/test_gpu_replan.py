@@ -15,7 +15,7 @@ def test_replan_matches_device_path(engine):
     prof = synthetic_profile("efficientnet")
     sc = engine.calibrate(prof, 64, 350.0, 0.5)
     ap = bench.anneal_params(24)
-    starts = bench.make_starts(engine, prof, 11, 0, 40)
+    starts = bench.make_starts(prof, 11, 0, 40, 0.75)
     res, best_w, final_w, record = engine.replan(starts, prof, sc, ap, 7, chain_base=40, cluster=0)
     b = engine.anneal(starts, prof, sc, ap, 7, chain_base=40, cluster=0)
     rec = engine.select_chains(b)

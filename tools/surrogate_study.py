@@ -104,6 +104,50 @@ def models(inst, R):
     if kq is None:
         kq = [e for e in order if w[e] > 0][-1]
     out["w0R_q"] = lat[kq] * fac
+    # stochastic families: mixture quantile with the same shares (rate_j / R)
+    share = 1000.0 * w / (mean + W0) / R
+    dist = SIM.edges[0].dist
+    sig = SIM.edges[0].sigma
+    from math import erfc, log, sqrt, exp
+    def surv(e, L):
+        if dist == 0:
+            return 1.0 if mean[e] > L else 0.0
+        if dist == 1:
+            return exp(-L / mean[e])
+        mu = log(mean[e]) - 0.5 * sig * sig
+        return 0.5 * erfc((log(L) - mu) / (sig * sqrt(2.0)))
+    if dist == 0:
+        out["mix_exact"] = out["w0R_q"]
+        out["mix_edge"] = out["w0R_q"]
+    else:
+        lo, hi = 1e-3, 1e5
+        for _ in range(100):
+            mid = sqrt(lo * hi)
+            t = sum(share[e] * surv(e, mid) for e in range(E) if w[e] > 0)
+            if t > 0.05:
+                lo = mid
+            else:
+                hi = mid
+        out["mix_exact"] = hi * fac
+        # boundary edge + within-edge conditional quantile
+        Tprev = 0.0
+        val = None
+        for e in order:
+            if w[e] <= 0:
+                continue
+            if Tprev + share[e] > 0.05:
+                p = 1.0 - (0.05 - Tprev) / share[e]
+                if dist == 1:
+                    val = mean[e] * (-log(1.0 - p))
+                else:
+                    from statistics import NormalDist
+                    mu = log(mean[e]) - 0.5 * sig * sig
+                    val = exp(mu + sig * NormalDist().inv_cdf(p))
+                break
+            Tprev += share[e]
+        if val is None:
+            val = lat[order[-1]]
+        out["mix_edge"] = val * fac
     return out
 
 
@@ -134,7 +178,7 @@ def main():
     CB = s_b * (1.0 - 0.7) / 0.7
     mb = models(base, R)
     ms = [models(f, R) for f in pops]
-    for key in ("lmax", "thr_q", "cnt_q", "idle_q", "c_q", "w0_q", "w0R_q"):
+    for key in ("lmax", "thr_q", "cnt_q", "idle_q", "c_q", "w0_q", "w0R_q", "mix_exact", "mix_edge"):
         L = np.array([x[key] for x in ms])
         s_s = L <= mb[key]
         s_d = dP <= lt_des
