@@ -16,6 +16,14 @@ from .evaluator import base_graph, calibrate, evaluate_one
 from .rng import derive_seed
 
 
+def _chain_job(args):
+    return anneal_chain(*args)
+
+
+def _serial_map(fn, jobs):
+    return [fn(j) for j in jobs]
+
+
 def intensity_at(samples, t):
     val = samples[0][1]
     for ts, c in samples:
@@ -27,7 +35,8 @@ def intensity_at(samples, t):
 
 
 def run_trace_clover(samples, n, profile, tables, lam, ap, seed, chains, feas, step_s=300.0, threshold=0.05,
-                     utilization=0.7, pue=1.5):
+                     utilization=0.7, pue=1.5, map_fn=None, chain_base=0):
+    """map_fn(fn, args) runs a re-plan's independent chains, e.g. a process pool's map."""
     ci_mean = sum(c for _, c in samples) / len(samples)
     base_sc = calibrate(profile, tables, n, ci_mean, lam, utilization, ci_base=ci_mean, pue=pue)
     V = tables.V
@@ -45,7 +54,8 @@ def run_trace_clover(samples, n, profile, tables, lam, ap, seed, chains, feas, s
         if prev <= 0 or abs(ci - prev) / prev > threshold:
             replanned = True
             s = derive_seed(seed, tick)
-            res = [anneal_chain(w, n, tables, sc, ap, s, c, feas) for c in range(chains)]
+            jobs = [(w, n, tables, sc, ap, s, chain_base + c, feas) for c in range(chains)]
+            res = (map_fn or _serial_map)(_chain_job, jobs)
             keys = [(0 if r.best["sla"] else 1, r.best["h"], c) for c, r in enumerate(res) if r.status >= 0]
             _, _, c = min(keys)
             cand = res[c]
