@@ -126,6 +126,40 @@ def exchange_record(engine: CloverEngine, record, group=None):
     return engine.reduce_records(gathered)
 
 
+def share_winner(record, res, best_w, chain_base: int, group=None):
+    """Every rank gets the global winner's chain-result row and best graph: the owning rank
+    (the one whose chains [chain_base, chain_base + len(res)) hold record.index) contributes
+    them, the others zeros, and one all-reduce (sum) of E + 10 int64 words delivers them."""
+    import torch
+    import torch.distributed as dist
+    E = best_w.shape[1]
+    local = int(record["index"]) - chain_base
+    words = np.zeros(10 + E, dtype=np.int64)
+    if 0 <= local < len(res):
+        words[:10] = np.frombuffer(res[local:local + 1].tobytes(), dtype=np.int64)
+        words[10:] = best_w[local].astype(np.int64)
+    t = torch.from_numpy(words)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, group=group)
+    words = t.cpu().numpy()
+    row = np.frombuffer(words[:10].tobytes(), dtype=CHAIN_DTYPE)[0]
+    return record, row, words[10:].astype(np.uint16)
+
+
+def exchange_winner(engine: CloverEngine, record, res, best_w, chain_base: int, group=None):
+    """Host record of this rank -> global winner record (all-gather + clv_reduce_records) ->
+    the winner's result row and graph on every rank (share_winner)."""
+    import torch
+    import torch.distributed as dist
+    raw = torch.from_numpy(np.frombuffer(np.asarray(record, dtype=RECORD_DTYPE).tobytes(), dtype=np.uint8).copy())
+    if dist.get_backend(group) == "nccl":
+        raw = raw.cuda()
+    g = exchange_record(engine, raw.to("cuda:%d" % engine.device) if not raw.is_cuda else raw, group)
+    rec = np.frombuffer(g.cpu().numpy().tobytes(), dtype=RECORD_DTYPE)[0].copy()
+    return share_winner(rec, res, best_w, chain_base, group)
+
+
 def _distributed(group, exchange: bool) -> bool:
     """True when the winner record must be exchanged across ranks."""
     if not exchange:
@@ -150,14 +184,20 @@ def anneal_chains(engine: CloverEngine, starts, profile: ProfileTable, scenarios
         starts = np.array([g.weights for g in starts], dtype=np.uint16)
     starts = np.ascontiguousarray(np.asarray(starts, dtype=np.uint16))
     n_chains, E = starts.shape
-    if not log and not _distributed(group, exchange):
-        # one native call: H2D, anneal, winner selection, D2H, synchronise (clv_replan)
+    if not log:
+        # one native call: H2D, anneal, winner selection, D2H, synchronise (clv_replan); with a
+        # process group the 32-byte local record is then exchanged and reduced in fixed order
+        # and the winning chain's graph and result row are shared by its owner
         res, best_w, final_w, record = engine.replan(starts, profile, scenarios, ap, seed, chain_base, cluster)
-        res, best_w, final_w = res.copy(), best_w.copy(), final_w.copy()
-        local = int(record["index"]) - chain_base
-        g = ConfigGraph(best_w[local].astype(np.int64), profile.variant_count, profile.name)
-        return ChainsResult(_result_from_chain(res[local], g), chain_base + local, res, best_w,
-                            final_w, int(res["evals"].sum()), record.copy(), None)
+        res, best_w, final_w, record = res.copy(), best_w.copy(), final_w.copy(), record.copy()
+        if _distributed(group, exchange):
+            record, row, w_best = exchange_winner(engine, record, res, best_w, chain_base, group)
+        else:
+            local = int(record["index"]) - chain_base
+            row, w_best = res[local], best_w[local]
+        g = ConfigGraph(np.asarray(w_best, dtype=np.int64), profile.variant_count, profile.name)
+        return ChainsResult(_result_from_chain(row, g), int(record["index"]), res, best_w,
+                            final_w, int(res["evals"].sum()), record, None)
     # H2D: cached pinned staging buffer -> cached device buffer (one async copy)
     nb_in = starts.nbytes
     h_in = engine.staging("ac_in_host", nb_in, pinned=True)
@@ -196,11 +236,13 @@ def anneal_chains(engine: CloverEngine, starts, profile: ProfileTable, scenarios
     if log_host is not None:
         log_arr = np.frombuffer(log_host.numpy().tobytes(), dtype=LOG_DTYPE)[:n_chains * steps].reshape(
             n_chains, steps)
-    local = int(record["index"]) - chain_base
-    if not 0 <= local < len(res):        # the winner lives on another rank: report ours
-        local = int(np.lexsort((np.arange(len(res)), res["h"], res["sla_met"] == 0))[0])
-    g = ConfigGraph(best_w[local].astype(np.int64), profile.variant_count, profile.name)
-    return ChainsResult(_result_from_chain(res[local], g), chain_base + local, res, best_w,
+    if _distributed(group, exchange):
+        _rec, row, w_best = share_winner(record, res, best_w, chain_base, group)
+    else:
+        local = int(record["index"]) - chain_base
+        row, w_best = res[local], best_w[local]
+    g = ConfigGraph(np.asarray(w_best, dtype=np.int64), profile.variant_count, profile.name)
+    return ChainsResult(_result_from_chain(row, g), int(record["index"]), res, best_w,
                         final_w, int(res["evals"].sum()), record, log_arr)
 
 
@@ -262,8 +304,9 @@ def blover_search(n: int, profile: ProfileTable, workload: Workload, ci: float, 
     ap = ap or AnnealParams(proposal="uniform", evaluate="proposal")
     sc = scenario_for(n, workload, ci, obj)
     seed = _seed_of(rng)
-    budget = max(1, math.ceil(ap.time_budget_s / ap.eval_cost_s)) if ap.eval_cost_s > 0 else ap.max_steps + 1
-    budget = min(budget, ap.max_steps + 1)
+    budget = ap.max_steps + 1
+    if ap.eval_cost_s > 0 and math.isfinite(ap.time_budget_s):
+        budget = min(budget, max(1, math.ceil(ap.time_budget_s / ap.eval_cost_s)))
     pods = [(profile, sc, n, 1.0)]
     _best, outs = eng.sweep(pods, 0, budget, seed, outputs=True)
     h = outs["h"].cpu().numpy()
