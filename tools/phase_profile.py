@@ -24,9 +24,9 @@ NAMES = ["prepare", "score", "cta_reduce", "sync1", "leader", "sync2", "apply"]
 
 eng = CloverEngine(n_max=64)
 prof = synthetic_profile("efficientnet")
-sc = eng.calibrate(prof, 64, 350.0, 0.5)
-st = bench.make_starts(eng, prof, bench.SEED, 0, 128)
-ap = AnnealParams(max_steps=64)
+sc = eng.calibrate(prof, bench.N_FLEET, bench.CI, bench.LAMBDA)
+st = bench.make_starts(prof, bench.SEED, 0, 128, 0.75)
+ap = bench.anneal_params(256)
 lib = N.load()
 lib.clv_debug_anneal_profile.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 cl = 3
