@@ -58,7 +58,8 @@ def idle_wait_ms(m, s1, s2, s3, R, R_q, inv, rho_c, tables):
     with a_k = sum w x^k, D = a2 m - a1^2, N0 = a1 a3 - a2^2, N1 = a1 a2 - a3 m the root
     solves R N0 W^2 - (R N1 + m N0) W + (R - a1) D = 0 (the cancellation-free branch of the
     quadratic formula).  Homogeneous fleets (D <= 1e-9 a2 m) and degenerate roots take
-    the homogeneous solution W = (m / R)(1 - rho); saturated fleets (rho >= 1) W = 0."""
+    the homogeneous solution W = (m / R)(1 - rho); saturated fleets (rho >= 1) W = 0.  W is clamped
+    to m / R (a bound of the exact root, so the kernels' screen may use 1000 m / R as W0's bound)."""
     t2, k2, t3, k3 = tables.rate_moment_rows()
     a1 = s1 * math.ldexp(1.0, -tables.kt)
     a2 = s2 * math.ldexp(1.0, -k2)
@@ -79,6 +80,8 @@ def idle_wait_ms(m, s1, s2, s3, R, R_q, inv, rho_c, tables):
         ok = (den > 0.0) & (root >= 0.0) & (root < np.inf) & ~(D <= (1e-9 * a2) * m)
         W = np.where(ok, root, homo)
         W = np.where(rho_c >= 1.0, 0.0, W)
+        mR = m * (1.0 / R)                    # W < m / R for the exact root; clamp the rounded one
+        W = np.where(W < mR, W, mR)
     return 1000.0 * W
 
 

@@ -39,6 +39,8 @@ constexpr int MAXP = CLV_MAX_EDGES * (CLV_MAX_EDGES + 1) / 2;   // 820 removal p
 constexpr int MAXCL = 16;
 constexpr long long NOIDX = -1;
 constexpr int NO_TOP = CLV_MAX_EDGES;     // lat_by_rank[NO_TOP] == 0: nothing left present
+constexpr int SCREEN_UNR = 2;             // candidates per lane per screen iteration
+constexpr int QCAP = 32 * (SCREEN_UNR + 1);   // per-warp queue: < 32 left + one iteration's survivors
 
 enum { MODE_BEST_ALL = 0, MODE_UNIFORM_ALL = 1, MODE_UNIFORM_PROPOSAL = 2 };
 
@@ -53,6 +55,10 @@ struct __align__(8) RemEnt {            // one removal multiset R (single edge o
     int end;                               // doubles: pre + move-list length
     int offm;                              // doubles: first static move-list entry minus pre
     int ibase;                             // canonical index base: E*E + P(r1,r2)*NP (doubles), r*E (singles)
+    // Screen bounds for every candidate of this removal (0 = none): when the pessimistic p95
+    // bound of the entry exceeds L_tail, all its candidates violate the SLA and
+    // h >= -f * penU (f >= 0) or h >= -f * penL (f < 0); see pess_bounds().
+    float penU, penL;
     unsigned short code;                   // slice code of R: sr1*125 + sr2*25 (doubles), sr*5 (singles)
     unsigned char r1, r2;                  // removed edges (r2 = 0xFF for singles)
     unsigned char k1, k2;                  // their latency ranks (k2 = 0xFF for singles)
@@ -110,8 +116,11 @@ struct __align__(16) AnnealSmem {
     unsigned magicE, magicNP;              // ceil(2^32 / E), ceil(2^32 / NP) (exact small divisions)
     unsigned char sl[CLV_MAX_EDGES];       // slice kind of the edge
     unsigned short pair_tab[MAXP];         // P -> (x | y << 8)
-    int pair_off[MAXP];                    // static move lists (staged from FamilyTables)
-    unsigned char pair_len[MAXP];
+    double ub[CLV_MAX_EDGES];              // per latency rank: c20 / (svc + W0_bound(m)) (pessimistic walk)
+    double Cd[CLV_MAX_EDGES];              // centre's pessimistic tail at its i-th highest present rank
+    unsigned char dr[CLV_MAX_EDGES];       // centre's present ranks, descending
+    int nDR;
+    unsigned long long seedS, seedO;       // screen thresholds known before scoring (keys of neighbours)
     // centre
     int w[CLV_MAX_EDGES];
     double S[6];
@@ -123,7 +132,10 @@ struct __align__(16) AnnealSmem {
     int nPE, nRP, nLen;
     unsigned char pe_list[CLV_MAX_EDGES];  // present edges, ascending
     int pfx[CLV_MAX_EDGES + 1];            // removal pairs starting before present edge i
-    int pk[MAXP];                          // available pair q: P | x << 10 | y << 16
+    union {
+        int pk[MAXP];                      // prepare: available pair q = P | x << 10 | y << 16
+        uint32_t qbuf[NWARP][QCAP];        // score: per-warp queue of screened-in candidates
+    };
     int warp_off[NWARP + 1], warp_len[NWARP + 1];
     int fsvec[CLV_K];                      // slice vector the feasibility bytes belong to
     unsigned char feasS[25];
@@ -134,6 +146,7 @@ struct __align__(16) AnnealSmem {
     KRec slS[2][MAXCL], slV[2][MAXCL], slP[2][MAXCL];   // [step parity][cluster rank]
     unsigned long long slc[2][MAXCL];
     int dec_done;
+    unsigned long long prof_surv;          // debug profile: screened-in double moves
     int bw[CLV_MAX_EDGES];                 // best graph (rank 0)
 };
 
@@ -252,6 +265,32 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
     s.pmask = m | ba1 | ba2;
 }
 
+// Screen bounds of one removal entry (ranks k1, k2 removed; -1 = none).  Pessimistic p95
+// walk: with the idle wait at its bound W0_b = 1000 m / R (>= the candidate's W0, the clamp in
+// idle_wait_ms), every present rank r contributes u_r = c20 / (svc_r + W0_b) per instance to
+// the tail, no more than its true share c20 / (svc_r + W0).  The centre's pessimistic tail
+// at its i-th highest present rank is Cd[i]; the removal subtracts u_k for each removed
+// instance at a rank k >= r; additions only add tail.  So if the pessimistic tail at rank r
+// exceeds 1 (with a 2^-30 margin that covers the rounding of the walk's P / Q fraction and
+// of these sums), the true walk of every candidate of this entry stops at a rank >= r:
+// p95 >= lat(r) =: lb, and L = p95 (1 + wq) >= lb.  When lb > L_tail every candidate of the
+// entry violates the SLA, and h = -f * (slo / L) >= -f * penU (f >= 0), h = -f * (L / slo) >=
+// -f * penL (f < 0, Eq. 6 amended), penU >= slo / lb and penL <= lb / slo rounded outwards.
+__device__ __forceinline__ void pess_bounds(const AnnealSmem &s, int k1, int k2, double slo, float &pu, float &pl) {
+    double lb = 0.0;
+    const int nd = s.nDR;
+    const double u1 = k1 >= 0 ? s.ub[k1] : 0.0, u2 = k2 >= 0 ? s.ub[k2] : 0.0;
+    for (int i = 0; i < nd; ++i) {
+        const int r = s.dr[i];
+        const double T = (s.Cd[i] - (k1 >= r ? u1 : 0.0)) - (k2 >= r ? u2 : 0.0);
+        if (T > 1.0 + 0x1p-30) { lb = s.lat_by_rank[r]; break; }
+    }
+    const float lf = __double2float_rd(lb);
+    const bool cv = (double)lf > slo;
+    pu = cv ? __double2float_ru((slo / (double)lf) * (1.0 + 0x1p-40)) : 0.0f;
+    pl = cv ? __double2float_rd(((double)lf / slo) * (1.0 - 0x1p-40)) : 0.0f;
+}
+
 // Per-step tables: deterministic ordered compaction of the removal pairs (every
 // CTA of the cluster must build identical tables because the cluster partitions
 // the move space by table position), the present-edge entries, and -- only when
@@ -259,7 +298,7 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
 // 625 double slice deltas (loads issued first so their latency overlaps the rest).
 template <bool PROF>
 __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, int n, const FeasView &F,
-                                             long long *pacc) {
+                                             const FamilyTables &T, double slo, long long *pacc) {
     const long long pt0 = PROF ? clock64() : 0;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int NP = E * (E + 1) / 2;
@@ -338,6 +377,30 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             pb += __shfl_sync(0xFFFFFFFFu, x, 31);
         }
         if (lane == 0) { s.nPE = k; s.pfx[k] = pb; s.nRP = pb; }
+        // the centre's present latency ranks, descending, with their pessimistic tails
+        // (suffix sums of w_r u_r over ranks >= r; lanes own ranks lane and lane + 32)
+        const unsigned long long pm = s.pmask;
+        const int rlo = lane, rhi = lane + 32;
+        const bool plo = (pm >> rlo) & 1ULL, phi = rhi < 64 && ((pm >> rhi) & 1ULL);
+        const double vlo = plo ? s.wr[rlo] * s.ub[rlo] : 0.0;
+        const double vhi = phi ? s.wr[rhi] * s.ub[rhi] : 0.0;
+        double shi = vhi, slo_ = vlo;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {            // suffix scans within each half
+            const double yh = __shfl_down_sync(0xFFFFFFFFu, shi, d);
+            const double yl = __shfl_down_sync(0xFFFFFFFFu, slo_, d);
+            if (lane + d < 32) { shi += yh; slo_ += yl; }
+        }
+        slo_ += __shfl_sync(0xFFFFFFFFu, shi, 0);     // + everything in the upper half
+        if (phi) {
+            const int i = __popcll(pm >> (rhi + 1));
+            s.dr[i] = (unsigned char)rhi; s.Cd[i] = shi;
+        }
+        if (plo) {
+            const int i = __popcll(pm >> (rlo + 1));
+            s.dr[i] = (unsigned char)rlo; s.Cd[i] = slo_;
+        }
+        if (lane == 0) s.nDR = __popcll(pm);
     }
     __syncthreads();
     const long long ptA = PROF ? clock64() : 0;
@@ -363,7 +426,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
                 const int y = s.pe_list[i + (q - s.pfx[i]) + (s.w[x] >= 2 ? 0 : 1)];
                 const int p = x * E - (x * (x - 1)) / 2 + (y - x);
                 s.pk[q] = p | (x << 10) | (y << 16);     // p < 1024; x, y < 64
-                lsum += s.pair_len[p];
+                lsum += __ldg(T.pair_len + p);
                 ++cnt;
             }
         }
@@ -414,9 +477,10 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
         r.k1 = s.rk[x]; r.k2 = s.rk[y];
         r.ibase = E * E + p * NP;
         r.pre = lpos;
-        r.offm = s.pair_off[p] - lpos;
-        lpos += s.pair_len[p];
+        r.offm = __ldg(T.pair_off + p) - lpos;
+        lpos += __ldg(T.pair_len + p);
         r.end = lpos;
+        pess_bounds(s, r.k1, r.k2, slo, r.penU, r.penL);
         r.code = (unsigned short)(s.sl[x] * 125 + s.sl[y] * 25);
         r.r1 = (unsigned char)x; r.r2 = (unsigned char)y;
     }
@@ -432,6 +496,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             r.ibase = e * E;
             r.code = (unsigned short)(s.sl[e] * 5);
             r.r1 = (unsigned char)e; r.r2 = 0xFF; r.offm = 0; r.end = 0; r.pre = 0;
+            r.penU = 0.0f; r.penL = 0.0f;             // singles are scored in full
         }
     }
     if (refresh && wid > 0) {
@@ -474,6 +539,138 @@ __device__ __forceinline__ void fold(const AnnealSmem &s, const AnnealArgs &args
         const unsigned long long hk = derive_seed4(seed, gchain, k, (uint64_t)idx + 1);
         if (krec_less(hk, idx, rP)) { rP.key = hk; rP.idx = idx; rP.hv = sc.h; }
     }
+}
+
+template <int EC>
+__device__ __forceinline__ const EvalConst &ec_of(const AnnealArgs &args, const AnnealSmem &s) {
+    if constexpr (EC == 2) return args.ec0;      // one scenario: constant-bank operands
+    else return s.ec;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x) {
+    const unsigned hi = __reduce_min_sync(0xFFFFFFFFu, (unsigned)(x >> 32));
+    const unsigned lo = __reduce_min_sync(0xFFFFFFFFu, (unsigned)(x >> 32) == hi ? (unsigned)x : 0xFFFFFFFFu);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
+// Full score of a queued double move (removal entry jj, position off in its move list).
+template <int MODE, int EC>
+__device__ __forceinline__ void score_queued(const AnnealSmem &s, const AnnealArgs &args, const RemEnt *rp,
+                                             const uint32_t *plist, uint32_t d, double mcnt, KRec &rS, KRec &rV,
+                                             KRec &rP, uint64_t gchain, uint64_t k) {
+    const RemEnt &R = rp[d & 0xFFFFu];
+    const uint32_t ent = __ldg(plist + R.offm + R.pre + (int)(d >> 16));
+    const int a1 = ent & 63, a2 = (ent >> 6) & 63;
+    const ARow &A1 = s.row[a1], &A2 = s.row[a2];
+    const CandWalk cw{&s, R.pm | s.rbit[a1] | s.rbit[a2], R.k1, R.k2, s.rk[a1], s.rk[a2]};
+    fold<MODE, EC>(s, args, R.b0 + A1.thr + A2.thr, R.b1 + A1.acc + A2.acc, R.b2 + A1.en + A2.en,
+                   R.b3 + A1.idle + A2.idle, R.b4 + A1.t2 + A2.t2, R.b5 + A1.t3 + A2.t3, cw, mcnt,
+                   R.ibase + (int)(ent >> 17), rS, rV, rP, args.seed, gchain, k);
+}
+
+// Double moves with an exact screen.  Each candidate first gets only A, E and f (the
+// epilogue's first half, the same ops and bits as the full score) and a lower bound of h:
+// h >= -f always (Eq. 6 amended: the SLA penalty only raises h; strict form, f < 0: h >= 0),
+// and h >= -f * pen for the entries whose pessimistic p95 bound already violates the SLA
+// (pess_bounds).  A candidate is scored in full only if its bound does not exceed a key
+// already achieved by a scored neighbour: the SLA class's for candidates that may meet the
+// SLA, the overall minimum's for certain violators (a violator above an achieved key is
+// neither the class minimum nor the overall minimum; when an SLA-meeting neighbour exists the
+// violating record is only compared against it).  In MODE_UNIFORM_ALL a candidate whose hash
+// could be the proposal is always scored (its h is the proposal's).  The thresholds start from
+// neighbours known before scoring (the previous centre, or the same neighbourhood when the
+// centre did not move) and tighten with the warp's records.  Survivors go to a per-warp queue
+// and are scored 32 at a time, so the full epilogue runs on full warps.  The records, and
+// hence every decision, are those of scoring every candidate in full.
+template <int MODE, int EC, bool PROF>
+__device__ __forceinline__ void score_doubles_screened(AnnealSmem &s, const AnnealArgs &args, const RemEnt *rp,
+                                                       const uint32_t *plist, int crank, int CL, KRec &rS, KRec &rV,
+                                                       KRec &rP, unsigned long long &cnt, uint64_t gchain, uint64_t k,
+                                                       long long *pacc) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int ND = s.nLen;
+    const int W = CL * NWARP;
+    const int chunk = (((ND + W - 1) / W) + 31) & ~31;
+    const int tb0 = (crank * NWARP + wid) * chunk;
+    const int tend = min(tb0 + chunk, ND);
+    if (tb0 >= ND) return;                       // warp-uniform
+    const EvalConst &cc = ec_of<EC>(args, s);
+    constexpr bool FAST = EC >= 1;
+    const double mcnt = s.mcount;
+    int lo = 0, hi = s.nRP - 1;
+    const int t0 = min(tb0 + lane, ND - 1);
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rp[mid].pre <= t0) lo = mid; else hi = mid - 1;
+    }
+    int j = lo;
+    uint32_t *q = s.qbuf[wid];
+    int qn = 0;
+    unsigned long long thS = s.seedS, thO = s.seedO, thP = ~0ULL;
+    {
+        const unsigned long long kS = warp_min_u64(rS.key), kV = warp_min_u64(rV.key);
+        thS = kS < thS ? kS : thS;
+        thO = kS < thO ? kS : thO;
+        thO = kV < thO ? kV : thO;
+        if (MODE == MODE_UNIFORM_ALL) thP = warp_min_u64(rP.key);
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    long long nsurv = 0;
+    for (int base = tb0; base < tend; base += 32 * SCREEN_UNR) {
+#pragma unroll
+        for (int u = 0; u < SCREEN_UNR; ++u) {
+            const int tu = base + 32 * u + lane;
+            bool sv = false;
+            uint32_t dsc = 0;
+            if (tu < tend) {
+                while (tu >= rp[j].end) ++j;
+                const RemEnt &R = rp[j];
+                const uint32_t ent = __ldg(plist + R.offm + tu);
+                if (s.feasD[R.code + ((ent >> 12) & 31)]) {
+                    ++cnt;
+                    const int a1 = ent & 63, a2 = (ent >> 6) & 63;
+                    const ARow &A1 = s.row[a1], &A2 = s.row[a2];
+                    const AER a = aer<FAST>(R.b0 + A1.thr + A2.thr, R.b1 + A1.acc + A2.acc, R.b2 + A1.en + A2.en,
+                                            R.b3 + A1.idle + A2.idle, cc);
+                    const double f = objective_f(a.A, a.E, cc);
+                    const bool neg_strict = f < 0.0 && cc.strict;
+                    double lb;
+                    unsigned long long th;
+                    if (R.penU > 0.0f) {             // every candidate of this entry violates the SLA
+                        lb = neg_strict ? 0.0 : -f * (double)(f >= 0.0 ? R.penU : R.penL);
+                        th = thO;
+                    } else {
+                        lb = neg_strict ? 0.0 : -f;
+                        th = thS;
+                    }
+                    sv = okey(lb) <= th;
+                    if (MODE == MODE_UNIFORM_ALL)
+                        sv = sv || derive_seed4(args.seed, gchain, k, (uint64_t)(R.ibase + (int)(ent >> 17)) + 1) <= thP;
+                    dsc = (uint32_t)j | ((uint32_t)(tu - R.pre) << 16);
+                }
+            }
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, sv);
+            if (sv) q[qn + __popc(bal & lt)] = dsc;
+            qn += __popc(bal);
+        }
+        __syncwarp();
+        while (qn >= 32) {
+            qn -= 32;
+            if (PROF) nsurv += 32;
+            score_queued<MODE, EC>(s, args, rp, plist, q[qn + lane], mcnt, rS, rV, rP, gchain, k);
+            const unsigned long long kS = warp_min_u64(rS.key), kV = warp_min_u64(rV.key);
+            thS = kS < thS ? kS : thS;
+            thO = kS < thO ? kS : thO;
+            thO = kV < thO ? kV : thO;
+            if (MODE == MODE_UNIFORM_ALL) { const unsigned long long kP = warp_min_u64(rP.key); thP = kP < thP ? kP : thP; }
+            __syncwarp();
+        }
+    }
+    if (qn > 0) {
+        if (PROF) nsurv += qn;
+        if (lane < qn) score_queued<MODE, EC>(s, args, rp, plist, q[lane], mcnt, rS, rV, rP, gchain, k);
+    }
+    if (PROF && lane == 0) atomicAdd(&s.prof_surv, (unsigned long long)nsurv);
 }
 
 // Optional phase profiler (CLV_ANNEAL_VARIANT=9): thread 0 of each CTA accumulates
@@ -521,7 +718,6 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     }
     for (int x = tid; x < E; x += ANT)
         for (int y = x; y < E; ++y) s.pair_tab[x * E - (x * (x - 1)) / 2 + (y - x)] = (unsigned short)(x | (y << 8));
-    for (int p = tid; p < E * (E + 1) / 2; p += ANT) { s.pair_off[p] = T.pair_off[p]; s.pair_len[p] = T.pair_len[p]; }
     if (tid == 0) {
         s.lat_by_rank[NO_TOP] = 0.0;
         s.mem_ok = T.mem_ok;
@@ -548,12 +744,18 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         int cnt = 0;
         for (int e = 0; e < E; ++e) { cnt += s.w[e]; s.wr[s.rk[e]] = (double)s.w[e]; }
         s.mcount = (double)cnt;
+        s.seedS = ~0ULL; s.seedO = ~0ULL; s.prof_surv = 0ULL;
     }
     __syncthreads();
+    {   // pessimistic per-instance tail shares (every GED move keeps m, so W0's bound is per chain)
+        const double w0b = w0_bound(s.mcount, s.ec);
+        for (int r = tid; r < E; r += ANT) s.ub[r] = s.ec.c20 / (s.svc_by_rank[r] + w0b);
+    }
 
     // ---- chain state: thread 0 of every CTA (identical everywhere); rank 0 writes outputs
     const bool leader = (crank == 0 && tid == 0);
     double hc = 0.0;
+    bool slac = false;                       // SLA class of the centre (MODE_BEST_ALL seeds)
     unsigned int bk1 = 0;
     unsigned long long bk2 = 0;
     int best_step = -1, stall = 0, steps = 0, status = 0;
@@ -570,6 +772,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         const Score sc = epilogue_d(s.S[0], s.S[1], s.S[2], s.S[3], s.S[4], s.S[5], s.mcount, s.ec,
                                     GraphWalk{&s, s.w, s.er, s.pmask});
         hc = sc.h;
+        slac = sc.sla;
         bk1 = sc.sla ? 0u : 1u; bk2 = okey(sc.h);
         for (int e = 0; e < E; ++e) s.bw[e] = s.w[e];
         s.dec_done = invalid || (args.max_steps <= 0);
@@ -590,7 +793,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             for (int q = 0; q < CLV_K; ++q) refreshed |= (s.svec[q] != s.fsvec[q]);
         }
         const long long prep0 = PROF ? clock64() : 0;
-        prepare_step<PROF>(s, rp, E, n, args.F, prof_acc);
+        prepare_step<PROF>(s, rp, E, n, args.F, T, s.ec.slo, prof_acc);
         if (PROF && threadIdx.x == 0 && refreshed) { prof_acc[7] += clock64() - prep0; prof_acc[8] += 1; }
         PROF_MARK(1);
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
@@ -616,7 +819,10 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         }
         // ---- doubles: flattened (removal entry, static list entry) space; each warp
         // owns a contiguous chunk, lanes walk it 32 apart (UNR independent items each)
-        {
+        if (MODE != MODE_UNIFORM_PROPOSAL) {
+            score_doubles_screened<MODE, EC, PROF>(s, args, rp, T.pair_list, crank, CL, rS, rV, rP, cnt, gchain,
+                                                   (uint64_t)k, prof_acc);
+        } else {
             const int lane = tid & 31, wid = tid >> 5;
             const int ND = s.nLen;
             const int W = CL * NWARP;
@@ -724,8 +930,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                     if (Sr.idx != 0x7FFFFFFF) { ck1 = 0u; ck2 = Sr.key; cidx = Sr.idx; }
                     else { ck1 = 1u; ck2 = Vr.key; cidx = Vr.idx; }
                     if (MODE == MODE_BEST_ALL) {
-                        const KRec &B = krec_less(Sr.key, Sr.idx, Vr) ? Sr : Vr;   // min h overall
-                        pidx = B.idx; hp = okey_inv(B.key);
+                        const bool bs = krec_less(Sr.key, Sr.idx, Vr);
+                        const KRec &B = bs ? Sr : Vr;   // min h overall
+                        pidx = B.idx; hp = okey_inv(B.key); slap = bs;
                     } else {
                         pidx = Pr.idx; hp = Pr.hv;
                     }
@@ -756,7 +963,19 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                     row.accepted = acc; row.new_best = nb; row.n_neighbours = (int)total;
                     args.log[(size_t)chain * args.max_steps + k] = row;
                 }
-                if (acc) { hc = hp; mv = pidx; }
+                // screen seeds for the next step: GED moves are symmetric, so after a move the
+                // previous centre (h = hc, class slac) is a neighbour of the new centre; without
+                // a move the next neighbourhood is this one and its records are achieved keys
+                if (MODE != MODE_UNIFORM_PROPOSAL) {
+                    if (acc) {
+                        s.seedO = okey(hc);
+                        s.seedS = (MODE == MODE_BEST_ALL && slac) ? okey(hc) : ~0ULL;
+                    } else {
+                        s.seedS = Sr.idx != 0x7FFFFFFF ? Sr.key : ~0ULL;
+                        s.seedO = krec_less(Sr.key, Sr.idx, Vr) ? Sr.key : Vr.key;
+                    }
+                }
+                if (acc) { hc = hp; mv = pidx; slac = slap; }
                 if (leader) args.mvlog[(size_t)chain * args.max_steps + k] = (int)mv;
                 steps = k + 1;
                 if (stall >= args.stall_limit) { status = 1; fin = 1; }
@@ -775,6 +994,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     }
     // Keep every CTA's shared memory alive until no peer can touch it over DSMEM.
     cluster.sync();
+    if (PROF && threadIdx.x == 0) prof_acc[16] = (long long)s.prof_surv;
     if (PROF && threadIdx.x == 0 && args.prof)
         for (int q = 0; q < PROF_SLOTS; ++q) args.prof[((size_t)blockIdx.x) * PROF_SLOTS + q] = prof_acc[q];
 

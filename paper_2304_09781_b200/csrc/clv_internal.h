@@ -123,7 +123,7 @@ __device__ inline void grid_finish(RecP r0, RecP r1, unsigned long long c0, unsi
     }
 }
 
-constexpr int PROF_SLOTS = 16;          // debug phase-profile slots per CTA (CLV_ANNEAL_VARIANT=9)
+constexpr int PROF_SLOTS = 20;          // debug phase-profile slots per CTA (CLV_ANNEAL_VARIANT=9)
 
 struct AnnealArgs {
     const FamilyTables *fam;

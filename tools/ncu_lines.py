@@ -34,8 +34,18 @@ for r in data:
     ln = off2line.get(a - base, ('?', 0))
     agg[ln] = agg.get(ln, 0) + n
     tot += n
-src = open(srcfile).read().split('\n')
+import os
+srcdir = os.path.dirname(os.path.abspath(srcfile))
+_cache = {}
+def src_line(f, l):
+    if f not in _cache:
+        try:
+            _cache[f] = open(os.path.join(srcdir, f)).read().split('\n')
+        except OSError:
+            _cache[f] = []
+    s = _cache[f]
+    return s[l - 1].strip()[:90] if 0 < l <= len(s) else ''
 print("total warp-level instructions", tot)
 for (f, l), n in sorted(agg.items(), key=lambda x: -x[1])[:int(sys.argv[5]) if len(sys.argv) > 5 else 40]:
-    s = src[l - 1].strip()[:90] if f == srcfile.split('/')[-1] and l > 0 else ''
+    s = src_line(f, l)
     print("%5.2f%% %-22s %4d  %s" % (100.0 * n / tot, f, l, s))

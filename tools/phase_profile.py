@@ -19,7 +19,7 @@ from paper_2304_09781_b200.engine import CloverEngine  # noqa: E402
 from paper_2304_09781_b200.objective import AnnealParams  # noqa: E402
 from paper_2304_09781_b200.profiles import synthetic_profile  # noqa: E402
 
-SLOTS = 16
+SLOTS = 20
 NAMES = ["prepare", "score", "cta_reduce", "sync1", "leader", "sync2", "apply"]
 
 eng = CloverEngine(n_max=64)
@@ -51,3 +51,6 @@ print("  of which thread 0 until the present-edge list starts (refresh issue / w
 print("feasibility refresh in %.1f%% of steps; prepare cycles per refresh step %d, per other step %d"
       % (100.0 * nref / steps.sum(), buf[:, 0, 7].sum() / max(nref, 1),
          (buf[:, 0, 0].sum() - buf[:, 0, 7].sum()) / max(steps.sum() - nref, 1)))
+surv = buf[:, :, 16].sum()
+ev = b.host()["results"]["evals"].astype(np.float64).sum()
+print("screen: %d double moves scored in full of %d candidates (%.2f%%)" % (surv, ev, 100.0 * surv / ev))
