@@ -116,11 +116,13 @@ struct __align__(16) AnnealSmem {
     unsigned magicE, magicNP;              // ceil(2^32 / E), ceil(2^32 / NP) (exact small divisions)
     unsigned char sl[CLV_MAX_EDGES];       // slice kind of the edge
     unsigned short pair_tab[MAXP];         // P -> (x | y << 8)
+    unsigned char pair_len[MAXP];          // static move-list lengths (staged from FamilyTables)
     double ub[CLV_MAX_EDGES];              // per latency rank: c20 / (svc + W0_bound(m)) (pessimistic walk)
     double Cd[CLV_MAX_EDGES];              // centre's pessimistic tail at its i-th highest present rank
     unsigned char dr[CLV_MAX_EDGES];       // centre's present ranks, descending
     int nDR;
     unsigned long long seedS, seedO;       // screen thresholds known before scoring (keys of neighbours)
+    unsigned long long thS_sh, thO_sh;     // CTA-wide screen thresholds of the current step
     // centre
     int w[CLV_MAX_EDGES];
     double S[6];
@@ -426,7 +428,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
                 const int y = s.pe_list[i + (q - s.pfx[i]) + (s.w[x] >= 2 ? 0 : 1)];
                 const int p = x * E - (x * (x - 1)) / 2 + (y - x);
                 s.pk[q] = p | (x << 10) | (y << 16);     // p < 1024; x, y < 64
-                lsum += __ldg(T.pair_len + p);
+                lsum += s.pair_len[p];
                 ++cnt;
             }
         }
@@ -478,7 +480,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
         r.ibase = E * E + p * NP;
         r.pre = lpos;
         r.offm = __ldg(T.pair_off + p) - lpos;
-        lpos += __ldg(T.pair_len + p);
+        lpos += s.pair_len[p];
         r.end = lpos;
         pess_bounds(s, r.k1, r.k2, slo, r.penU, r.penL);
         r.code = (unsigned short)(s.sl[x] * 125 + s.sl[y] * 25);
@@ -496,7 +498,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             r.ibase = e * E;
             r.code = (unsigned short)(s.sl[e] * 5);
             r.r1 = (unsigned char)e; r.r2 = 0xFF; r.offm = 0; r.end = 0; r.pre = 0;
-            r.penU = 0.0f; r.penL = 0.0f;             // singles are scored in full
+            pess_bounds(s, r.k1, -1, slo, r.penU, r.penL);
         }
     }
     if (refresh && wid > 0) {
@@ -553,11 +555,21 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x)
     return ((unsigned long long)hi << 32) | lo;
 }
 
-// Full score of a queued double move (removal entry jj, position off in its move list).
+// Full score of a queued move: bit 31 set = single (present-edge entry i, target edge a),
+// else double (removal entry jj, position off in its static move list).
 template <int MODE, int EC>
 __device__ __forceinline__ void score_queued(const AnnealSmem &s, const AnnealArgs &args, const RemEnt *rp,
                                              const uint32_t *plist, uint32_t d, double mcnt, KRec &rS, KRec &rV,
                                              KRec &rP, uint64_t gchain, uint64_t k) {
+    if (d >> 31) {
+        const RemEnt &R = s.se[(d >> 8) & 0xFFu];
+        const int a = d & 0xFFu;
+        const ARow &A = s.row[a];
+        const CandWalk cw{&s, R.pm | s.rbit[a], R.k1, 0xFF, s.rk[a], 0xFF};
+        fold<MODE, EC>(s, args, R.b0 + A.thr, R.b1 + A.acc, R.b2 + A.en, R.b3 + A.idle, R.b4 + A.t2, R.b5 + A.t3,
+                       cw, mcnt, R.ibase + a, rS, rV, rP, args.seed, gchain, k);
+        return;
+    }
     const RemEnt &R = rp[d & 0xFFFFu];
     const uint32_t ent = __ldg(plist + R.offm + R.pre + (int)(d >> 16));
     const int a1 = ent & 63, a2 = (ent >> 6) & 63;
@@ -568,92 +580,55 @@ __device__ __forceinline__ void score_queued(const AnnealSmem &s, const AnnealAr
                    R.ibase + (int)(ent >> 17), rS, rV, rP, args.seed, gchain, k);
 }
 
-// Double moves with an exact screen.  Each candidate first gets only A, E and f (the
-// epilogue's first half, the same ops and bits as the full score) and a lower bound of h:
-// h >= -f always (Eq. 6 amended: the SLA penalty only raises h; strict form, f < 0: h >= 0),
-// and h >= -f * pen for the entries whose pessimistic p95 bound already violates the SLA
-// (pess_bounds).  A candidate is scored in full only if its bound does not exceed a key
+__device__ __forceinline__ double key_limit(unsigned long long th) {   // okey(x) <= th  <=>  x <= key_limit(th)
+    return th == ~0ULL ? __longlong_as_double(0x7FF0000000000000LL) : okey_inv(th);
+}
+
+// Lower bound of h for the screen (see score_screened); a, f: the candidate's A/E and f.
+__device__ __forceinline__ bool screen_keep(double f, const RemEnt &R, bool strict, double limS, double limO) {
+    const bool neg_strict = f < 0.0 && strict;
+    double lb, lim;
+    if (R.penU > 0.0f) {                         // every candidate of this entry violates the SLA
+        lb = neg_strict ? 0.0 : -f * (double)(f >= 0.0 ? R.penU : R.penL);
+        lim = limO;
+    } else {
+        lb = neg_strict ? 0.0 : -f;
+        lim = limS;
+    }
+    return lb <= lim;
+}
+
+// Single and double moves with an exact screen.  Each candidate first gets only A, E and f
+// (the epilogue's first half, the same ops and bits as the full score) and a lower bound of
+// h: h >= -f always (Eq. 6 amended: the SLA penalty only raises h; strict form, f < 0: h >= 0),
+// and h >= -f * pen for the removal entries whose pessimistic p95 bound already violates the
+// SLA (pess_bounds).  A candidate is scored in full only if its bound does not exceed a key
 // already achieved by a scored neighbour: the SLA class's for candidates that may meet the
 // SLA, the overall minimum's for certain violators (a violator above an achieved key is
 // neither the class minimum nor the overall minimum; when an SLA-meeting neighbour exists the
 // violating record is only compared against it).  In MODE_UNIFORM_ALL a candidate whose hash
 // could be the proposal is always scored (its h is the proposal's).  The thresholds start from
 // neighbours known before scoring (the previous centre, or the same neighbourhood when the
-// centre did not move) and tighten with the warp's records.  Survivors go to a per-warp queue
+// centre did not move) and tighten with the CTA's records.  Survivors go to a per-warp queue
 // and are scored 32 at a time, so the full epilogue runs on full warps.  The records, and
 // hence every decision, are those of scoring every candidate in full.
 template <int MODE, int EC, bool PROF>
-__device__ __forceinline__ void score_doubles_screened(AnnealSmem &s, const AnnealArgs &args, const RemEnt *rp,
-                                                       const uint32_t *plist, int crank, int CL, KRec &rS, KRec &rV,
-                                                       KRec &rP, unsigned long long &cnt, uint64_t gchain, uint64_t k,
-                                                       long long *pacc) {
+__device__ __forceinline__ void score_screened(AnnealSmem &s, const AnnealArgs &args, const RemEnt *rp,
+                                               const uint32_t *plist, int crank, int CL, KRec &rS, KRec &rV,
+                                               KRec &rP, unsigned long long &cnt, uint64_t gchain, uint64_t k) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int ND = s.nLen;
-    const int W = CL * NWARP;
-    const int chunk = (((ND + W - 1) / W) + 31) & ~31;
-    const int tb0 = (crank * NWARP + wid) * chunk;
-    const int tend = min(tb0 + chunk, ND);
-    if (tb0 >= ND) return;                       // warp-uniform
     const EvalConst &cc = ec_of<EC>(args, s);
     constexpr bool FAST = EC >= 1;
+    const bool strict = cc.strict != 0;
     const double mcnt = s.mcount;
-    int lo = 0, hi = s.nRP - 1;
-    const int t0 = min(tb0 + lane, ND - 1);
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (rp[mid].pre <= t0) lo = mid; else hi = mid - 1;
-    }
-    int j = lo;
+    const int E = args.E;
     uint32_t *q = s.qbuf[wid];
     int qn = 0;
-    unsigned long long thS = s.seedS, thO = s.seedO, thP = ~0ULL;
-    {
-        const unsigned long long kS = warp_min_u64(rS.key), kV = warp_min_u64(rV.key);
-        thS = kS < thS ? kS : thS;
-        thO = kS < thO ? kS : thO;
-        thO = kV < thO ? kV : thO;
-        if (MODE == MODE_UNIFORM_ALL) thP = warp_min_u64(rP.key);
-    }
+    unsigned long long thS = s.thS_sh, thO = s.thO_sh, thP = ~0ULL;
+    double limS = key_limit(thS), limO = key_limit(thO);
     const unsigned lt = (1u << lane) - 1u;
     long long nsurv = 0;
-    for (int base = tb0; base < tend; base += 32 * SCREEN_UNR) {
-#pragma unroll
-        for (int u = 0; u < SCREEN_UNR; ++u) {
-            const int tu = base + 32 * u + lane;
-            bool sv = false;
-            uint32_t dsc = 0;
-            if (tu < tend) {
-                while (tu >= rp[j].end) ++j;
-                const RemEnt &R = rp[j];
-                const uint32_t ent = __ldg(plist + R.offm + tu);
-                if (s.feasD[R.code + ((ent >> 12) & 31)]) {
-                    ++cnt;
-                    const int a1 = ent & 63, a2 = (ent >> 6) & 63;
-                    const ARow &A1 = s.row[a1], &A2 = s.row[a2];
-                    const AER a = aer<FAST>(R.b0 + A1.thr + A2.thr, R.b1 + A1.acc + A2.acc, R.b2 + A1.en + A2.en,
-                                            R.b3 + A1.idle + A2.idle, cc);
-                    const double f = objective_f(a.A, a.E, cc);
-                    const bool neg_strict = f < 0.0 && cc.strict;
-                    double lb;
-                    unsigned long long th;
-                    if (R.penU > 0.0f) {             // every candidate of this entry violates the SLA
-                        lb = neg_strict ? 0.0 : -f * (double)(f >= 0.0 ? R.penU : R.penL);
-                        th = thO;
-                    } else {
-                        lb = neg_strict ? 0.0 : -f;
-                        th = thS;
-                    }
-                    sv = okey(lb) <= th;
-                    if (MODE == MODE_UNIFORM_ALL)
-                        sv = sv || derive_seed4(args.seed, gchain, k, (uint64_t)(R.ibase + (int)(ent >> 17)) + 1) <= thP;
-                    dsc = (uint32_t)j | ((uint32_t)(tu - R.pre) << 16);
-                }
-            }
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, sv);
-            if (sv) q[qn + __popc(bal & lt)] = dsc;
-            qn += __popc(bal);
-        }
-        __syncwarp();
+    auto drain = [&](bool all) {                 // score queued survivors 32 at a time
         while (qn >= 32) {
             qn -= 32;
             if (PROF) nsurv += 32;
@@ -663,13 +638,126 @@ __device__ __forceinline__ void score_doubles_screened(AnnealSmem &s, const Anne
             thO = kS < thO ? kS : thO;
             thO = kV < thO ? kV : thO;
             if (MODE == MODE_UNIFORM_ALL) { const unsigned long long kP = warp_min_u64(rP.key); thP = kP < thP ? kP : thP; }
+            if (lane == 0) { atomicMin(&s.thS_sh, thS); atomicMin(&s.thO_sh, thO); }
+            limS = key_limit(thS); limO = key_limit(thO);
             __syncwarp();
         }
+        if (all && qn > 0) {
+            if (PROF) nsurv += qn;
+            if (lane < qn) score_queued<MODE, EC>(s, args, rp, plist, q[lane], mcnt, rS, rV, rP, gchain, k);
+            qn = 0;
+        }
+    };
+    auto refresh = [&]() {                       // the CTA's best achieved keys so far
+        const unsigned long long a = *(volatile unsigned long long *)&s.thS_sh;
+        const unsigned long long b = *(volatile unsigned long long *)&s.thO_sh;
+        if (a < thS) { thS = a; limS = key_limit(thS); }
+        if (b < thO) { thO = b; limO = key_limit(thO); }
+    };
+    // ---- singles (present edge i, target edge a), strided over the cluster's threads
+    {
+        const int nS = s.nPE * E;
+        const unsigned long long mem_ok = s.mem_ok;
+        for (int base = (crank * NWARP + wid) * 32; base < nS; base += CL * ANT) {
+            const int t = base + lane;
+            bool sv = false;
+            uint32_t dsc = 0;
+            if (t < nS) {
+                const int i = t / E, a = t - (t / E) * E;
+                const RemEnt &R = s.se[i];
+                if (a != R.r1 && ((mem_ok >> a) & 1ULL) && s.feasS[R.code + s.sl[a]]) {
+                    ++cnt;
+                    const ARow &A = s.row[a];
+                    const AER ae = aer<FAST>(R.b0 + A.thr, R.b1 + A.acc, R.b2 + A.en, R.b3 + A.idle, cc);
+                    sv = screen_keep(objective_f(ae.A, ae.E, cc), R, strict, limS, limO);
+                    if (MODE == MODE_UNIFORM_ALL)
+                        sv = sv || derive_seed4(args.seed, gchain, k, (uint64_t)(R.ibase + a) + 1) <= thP;
+                    dsc = 0x80000000u | ((uint32_t)i << 8) | (uint32_t)a;
+                }
+            }
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, sv);
+            if (sv) q[qn + __popc(bal & lt)] = dsc;
+            qn += __popc(bal);
+            __syncwarp();
+            drain(false);
+        }
+        // score the surviving singles now: their records set the doubles' thresholds
+        drain(true);
+        const unsigned long long kS = warp_min_u64(rS.key), kV = warp_min_u64(rV.key);
+        thS = kS < thS ? kS : thS;
+        thO = kS < thO ? kS : thO;
+        thO = kV < thO ? kV : thO;
+        if (MODE == MODE_UNIFORM_ALL) { const unsigned long long kP = warp_min_u64(rP.key); thP = kP < thP ? kP : thP; }
+        if (lane == 0) { atomicMin(&s.thS_sh, thS); atomicMin(&s.thO_sh, thO); }
+        limS = key_limit(thS); limO = key_limit(thO);
+        __syncwarp();
     }
-    if (qn > 0) {
-        if (PROF) nsurv += qn;
-        if (lane < qn) score_queued<MODE, EC>(s, args, rp, plist, q[lane], mcnt, rS, rV, rP, gchain, k);
+    // ---- doubles: flattened (removal entry, static list entry) space; each warp owns a
+    // contiguous chunk, lanes walk it 32 apart (SCREEN_UNR items per lane and iteration)
+    const int ND = s.nLen;
+    const int W = CL * NWARP;
+    const int chunk = (((ND + W - 1) / W) + 31) & ~31;
+    const int tb0 = (crank * NWARP + wid) * chunk;
+    const int tend = min(tb0 + chunk, ND);
+    if (tb0 < ND) {                              // warp-uniform
+        int lo = 0, hi = s.nRP - 1;
+        const int t0 = min(tb0 + lane, ND - 1);
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (rp[mid].pre <= t0) lo = mid; else hi = mid - 1;
+        }
+        int j = lo;
+        // software pipeline: the move-list words of the next iteration are loaded (L2 latency)
+        // while the current iteration is screened
+        uint32_t entn[SCREEN_UNR];
+        int jn[SCREEN_UNR];
+        auto fetch = [&](int b) {
+#pragma unroll
+            for (int u = 0; u < SCREEN_UNR; ++u) {
+                const int tu = min(b + 32 * u + lane, tend - 1);
+                while (tu >= rp[j].end) ++j;
+                jn[u] = j;
+                entn[u] = __ldg(plist + rp[j].offm + tu);
+            }
+        };
+        fetch(tb0);
+        for (int base = tb0; base < tend; base += 32 * SCREEN_UNR) {
+            refresh();
+            uint32_t ent[SCREEN_UNR];
+            int jc[SCREEN_UNR];
+#pragma unroll
+            for (int u = 0; u < SCREEN_UNR; ++u) { ent[u] = entn[u]; jc[u] = jn[u]; }
+            if (base + 32 * SCREEN_UNR < tend) fetch(base + 32 * SCREEN_UNR);
+            bool sv[SCREEN_UNR];
+            uint32_t dsc[SCREEN_UNR];
+#pragma unroll
+            for (int u = 0; u < SCREEN_UNR; ++u) {
+                const int tu = base + 32 * u + lane;
+                const RemEnt &R = rp[jc[u]];
+                const uint32_t e = ent[u];
+                const bool ok = tu < tend && s.feasD[R.code + ((e >> 12) & 31)];
+                cnt += ok ? 1 : 0;
+                const int a1 = e & 63, a2 = (e >> 6) & 63;
+                const ARow &A1 = s.row[a1], &A2 = s.row[a2];
+                const AER ae = aer<FAST>(R.b0 + A1.thr + A2.thr, R.b1 + A1.acc + A2.acc,
+                                         R.b2 + A1.en + A2.en, R.b3 + A1.idle + A2.idle, cc);
+                bool keep = screen_keep(objective_f(ae.A, ae.E, cc), R, strict, limS, limO);
+                if (MODE == MODE_UNIFORM_ALL)
+                    keep = keep || derive_seed4(args.seed, gchain, k, (uint64_t)(R.ibase + (int)(e >> 17)) + 1) <= thP;
+                sv[u] = ok && keep;
+                dsc[u] = (uint32_t)jc[u] | ((uint32_t)(tu - R.pre) << 16);
+            }
+#pragma unroll
+            for (int u = 0; u < SCREEN_UNR; ++u) {
+                const unsigned bal = __ballot_sync(0xFFFFFFFFu, sv[u]);
+                if (sv[u]) q[qn + __popc(bal & lt)] = dsc[u];
+                qn += __popc(bal);
+            }
+            __syncwarp();
+            drain(false);
+        }
     }
+    drain(true);
     if (PROF && lane == 0) atomicAdd(&s.prof_surv, (unsigned long long)nsurv);
 }
 
@@ -716,6 +804,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         s.er[e] = T.edge_by_rank[e];
         s.sl[e] = (unsigned char)(e % 5);
     }
+    for (int p = tid; p < E * (E + 1) / 2; p += ANT) s.pair_len[p] = T.pair_len[p];
     for (int x = tid; x < E; x += ANT)
         for (int y = x; y < E; ++y) s.pair_tab[x * E - (x * (x - 1)) / 2 + (y - x)] = (unsigned short)(x | (y << 8));
     if (tid == 0) {
@@ -745,6 +834,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         for (int e = 0; e < E; ++e) { cnt += s.w[e]; s.wr[s.rk[e]] = (double)s.w[e]; }
         s.mcount = (double)cnt;
         s.seedS = ~0ULL; s.seedO = ~0ULL; s.prof_surv = 0ULL;
+        s.thS_sh = ~0ULL; s.thO_sh = ~0ULL;
     }
     __syncthreads();
     {   // pessimistic per-instance tail shares (every GED move keeps m, so W0's bound is per chain)
@@ -799,7 +889,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
         unsigned long long cnt = 0;
         // ---- singles: (present edge i, target edge a), strided over the cluster
-        {
+        // (scored modes: screened with the doubles in score_screened)
+        if (MODE == MODE_UNIFORM_PROPOSAL) {
             const int nS = s.nPE * E;
             int i = gt / E, a = gt - (gt / E) * E;
             const int dI = G / E, dA = G - (G / E) * E;
@@ -820,8 +911,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         // ---- doubles: flattened (removal entry, static list entry) space; each warp
         // owns a contiguous chunk, lanes walk it 32 apart (UNR independent items each)
         if (MODE != MODE_UNIFORM_PROPOSAL) {
-            score_doubles_screened<MODE, EC, PROF>(s, args, rp, T.pair_list, crank, CL, rS, rV, rP, cnt, gchain,
-                                                   (uint64_t)k, prof_acc);
+            score_screened<MODE, EC, PROF>(s, args, rp, T.pair_list, crank, CL, rS, rV, rP, cnt, gchain,
+                                           (uint64_t)k);
         } else {
             const int lane = tid & 31, wid = tid >> 5;
             const int ND = s.nLen;
@@ -975,6 +1066,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                         s.seedO = krec_less(Sr.key, Sr.idx, Vr) ? Sr.key : Vr.key;
                     }
                 }
+                s.thS_sh = s.seedS; s.thO_sh = s.seedO;
                 if (acc) { hc = hp; mv = pidx; slac = slap; }
                 if (leader) args.mvlog[(size_t)chain * args.max_steps + k] = (int)mv;
                 steps = k + 1;
