@@ -121,6 +121,8 @@ struct __align__(16) AnnealSmem {
     double Cd[CLV_MAX_EDGES];              // centre's pessimistic tail at its i-th highest present rank
     unsigned char dr[CLV_MAX_EDGES];       // centre's present ranks, descending
     int nDR;
+    int icb;                               // first i with Cd[i] > 1 + margin (the centre's bound rank)
+    float penUc, penLc;                    // pen factors of the centre's bound
     unsigned long long seedS, seedO;       // screen thresholds known before scoring (keys of neighbours)
     unsigned long long thS_sh, thO_sh;     // CTA-wide screen thresholds of the current step
     // centre
@@ -267,6 +269,8 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
     s.pmask = m | ba1 | ba2;
 }
 
+__device__ __forceinline__ void pen_factors(double lb, double slo, float &pu, float &pl);
+
 // Screen bounds of one removal entry (ranks k1, k2 removed; -1 = none).  Pessimistic p95
 // walk: with the idle wait at its bound W0_b = 1000 m / R (>= the candidate's W0, the clamp in
 // idle_wait_ms), every present rank r contributes u_r = c20 / (svc_r + W0_b) per instance to
@@ -279,6 +283,10 @@ __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
 // entry violates the SLA, and h = -f * (slo / L) >= -f * penU (f >= 0), h = -f * (L / slo) >=
 // -f * penL (f < 0, Eq. 6 amended), penU >= slo / lb and penL <= lb / slo rounded outwards.
 __device__ __forceinline__ void pess_bounds(const AnnealSmem &s, int k1, int k2, double slo, float &pu, float &pl) {
+    // Removals below the centre's own bound rank leave the tails at and above it unchanged:
+    // the centre's bound (and its pen factors) hold for the entry as they are.
+    const int ic = s.icb;
+    if (ic < s.nDR && k1 < s.dr[ic] && k2 < s.dr[ic]) { pu = s.penUc; pl = s.penLc; return; }
     double lb = 0.0;
     const int nd = s.nDR;
     const double u1 = k1 >= 0 ? s.ub[k1] : 0.0, u2 = k2 >= 0 ? s.ub[k2] : 0.0;
@@ -287,6 +295,10 @@ __device__ __forceinline__ void pess_bounds(const AnnealSmem &s, int k1, int k2,
         const double T = (s.Cd[i] - (k1 >= r ? u1 : 0.0)) - (k2 >= r ? u2 : 0.0);
         if (T > 1.0 + 0x1p-30) { lb = s.lat_by_rank[r]; break; }
     }
+    pen_factors(lb, slo, pu, pl);
+}
+
+__device__ __forceinline__ void pen_factors(double lb, double slo, float &pu, float &pl) {
     const float lf = __double2float_rd(lb);
     const bool cv = (double)lf > slo;
     pu = cv ? __double2float_ru((slo / (double)lf) * (1.0 + 0x1p-40)) : 0.0f;
@@ -403,6 +415,16 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             s.dr[i] = (unsigned char)rlo; s.Cd[i] = slo_;
         }
         if (lane == 0) s.nDR = __popcll(pm);
+        // the centre's bound rank: the highest present rank whose pessimistic tail exceeds 1
+        const bool bhi = phi && shi > 1.0 + 0x1p-30, blo = plo && slo_ > 1.0 + 0x1p-30;
+        const unsigned bh = __ballot_sync(0xFFFFFFFFu, bhi), bl = __ballot_sync(0xFFFFFFFFu, blo);
+        if (lane == 0) {
+            const int rb = bh ? 32 + (31 - __clz((int)bh)) : (bl ? 31 - __clz((int)bl) : -1);
+            s.icb = rb >= 0 ? __popcll(pm >> (rb + 1)) : 64;
+            float pu, pl;
+            pen_factors(rb >= 0 ? s.lat_by_rank[rb] : 0.0, slo, pu, pl);
+            s.penUc = pu; s.penLc = pl;
+        }
     }
     __syncthreads();
     const long long ptA = PROF ? clock64() : 0;
@@ -722,7 +744,7 @@ __device__ __forceinline__ void score_screened(AnnealSmem &s, const AnnealArgs &
         };
         fetch(tb0);
         for (int base = tb0; base < tend; base += 32 * SCREEN_UNR) {
-            refresh();
+            if (((base - tb0) & (4 * 32 * SCREEN_UNR - 1)) == 0) refresh();
             uint32_t ent[SCREEN_UNR];
             int jc[SCREEN_UNR];
 #pragma unroll
