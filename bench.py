@@ -512,18 +512,93 @@ def _timed_steps(fn, steps, warmup, flush):
     return [(a.elapsed_time(b), o) for a, b, o in ev[warmup:]]
 
 
+def flops_per_candidate(e_nz, k_walk):
+    """Algorithmic fp64 work of one candidate scored from scratch:
+    five weighted row sums over the E_nz present edges (10 E_nz), the idle sum over the five
+    slice kinds (10), the epilogue's fixed part (A, E, rho: 11; idle-queue wait incl. one sqrt
+    and one division: 30; L, Eqs. 1-3, 6: 22) and 7 per rank visited by the p95 walk."""
+    return 10.0 * e_nz + 73.0 + 7.0 * k_walk
+
+
+def _walk_stats(W, T, sc):
+    """Mean E_nz and p95-walk length of a sample of candidate graphs (oracle, measurement only)."""
+    from oracle.evaluator import walk_lengths
+    W = np.asarray(W, dtype=np.int64).reshape(-1, T.E)
+    return float((W > 0).sum(axis=1).mean()), float(walk_lengths(W, T, sc).mean())
+
+
+def _fp64_roofline(candidates_per_launch, seconds_per_launch, e_nz, k_walk, kernel, note):
+    peak, peak_src = fp64_peak_tflops()
+    if e_nz is None or not seconds_per_launch:
+        return {"bound": "fp64", "achieved": None, "peak": peak, "unit": "TFLOP/s", "frac": None, "traffic": None,
+                "kernel": kernel, "note": "no work sample (run without --no-cpu-baseline)"}
+    fl = flops_per_candidate(e_nz, k_walk)
+    ach = candidates_per_launch * fl / seconds_per_launch / 1e12
+    return {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak if peak else None,
+            "traffic": None, "traffic_note": "generated candidates: no per-candidate HBM traffic",
+            "kernel": kernel, "peak_source": peak_src,
+            "algorithmic": "%.1f fp64 flops per candidate (10 E_nz + 73 + 7 K; E_nz %.2f, walk K %.2f measured on the "
+                           "CPU sample) x %.4g candidates per launch; %s" % (fl, e_nz, k_walk, candidates_per_launch, note)}
+
+
+def _pool_map(fn, jobs, cores):
+    import multiprocessing as mp
+    with mp.get_context("fork").Pool(cores) as pool:
+        return pool.map(fn, jobs, chunksize=1)
+
+
+_C0 = {}
+
+
+def _c0_eval(rng):
+    from oracle.evaluator import evaluate
+    b, e = rng
+    ev = evaluate(_C0["W"][b:e], _C0["T"], _C0["sc"])
+    return ev.h, ev.f, ev.L, ev.sla
+
+
+def _c1_chain(a):
+    from oracle.anneal import anneal_chain
+    w0, lam_i, seed, max_steps = a
+    t0 = time.perf_counter()
+    out = anneal_chain(w0, 8, _C0["T"], _C0["scs"][lam_i], _C0["ap"], seed, lam_i, _C0["feas"])
+    return out, time.perf_counter() - t0
+
+
+def _c3_job(i):
+    return _C0["fn"](_C0["jobs"][i])
+
+
+def _c4_eval(rng):
+    from oracle.search import sweep_evaluate
+    b, e = rng
+    return sweep_evaluate(_C0["seed"], b, e, _C0["pods"], _C0["topo"])
+
+
 def run_other(args, rank, world, local):
-    """c0 (ORACLE, n=1), c1 (lambda sweep, n=8), c4 (10^9 two-pod sweep, n=256)."""
+    """c0 (ORACLE, n=1), c1 (lambda sweep, n=8), c3 (24-h trace), c4 (10^9 two-pod sweep, n=256), des.
+    Each line carries the device rate, an end-to-end rate through the public API (host in, host
+    out), and on rank 0 at N=1 the CPU oracle port on one core and on all cores, the parity of
+    the GPU result with it, and the fp64 roofline of the kernel."""
+    import ctypes
     import torch
     import torch.distributed as dist
+    from paper_2304_09781_b200 import _native as NAT
     from paper_2304_09781_b200.engine import CloverEngine
     from paper_2304_09781_b200.profiles import synthetic_profile
     from paper_2304_09781_b200.distributed import shard
     from paper_2304_09781_b200.search import exchange_record
+    from paper_2304_09781_b200.mig import DEFAULT_TOPOLOGY
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     eng = CloverEngine(device=local)
     extra = {}
+    cpu_on = rank == 0 and world == 1 and not args.no_cpu_baseline
+    cores = len(os.sched_getaffinity(0))
+    e2e, cpu, cpu_all, parity, roof = None, None, None, None, None
+    wsample = None
     if args.workload == "c0":
+        from paper_2304_09781_b200.sim import Workload
+        from paper_2304_09781_b200 import search as SR
         prof = synthetic_profile("efficientnet")
         sc = eng.calibrate(prof, 1, 400.0, 0.5)
         total = eng.oracle_size(prof)
@@ -534,6 +609,50 @@ def run_other(args, rank, world, local):
               "(%d candidates, sharded by index range)" % total
         extra["winner"] = eng.oracle_decode(prof, res[-1][1]["index"])
         scaling = "strong"
+        # e2e: the SPEC entry point, host scenario in, EvalResult out
+        wl = Workload(sc.arrival_rps, 600.0, SEED)
+        et = []
+        for s in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            SR.oracle_search(1, prof, wl, 400.0, sc.obj, engine=eng)
+            et.append(time.perf_counter() - t0)
+        e2e = {"value": total / (sum(et[args.warmup:]) / args.steps), "unit": UNIT,
+               "h2d_bytes_per_step": ctypes.sizeof(NAT.EvalParams), "d2h_bytes_per_step": ctypes.sizeof(NAT.Best),
+               "path": "search.oracle_search (SPEC signature) -> clv_oracle_search + clv_oracle_decode"}
+        if cpu_on:
+            from oracle.tables import OracleTables
+            from oracle.evaluator import calibrate
+            from oracle.search import oracle_graphs, select_oracle
+            T = OracleTables.from_profile(prof)
+            osc = calibrate(prof, T, 1, 400.0, 0.5)
+            t0 = time.perf_counter()
+            W = oracle_graphs(DEFAULT_TOPOLOGY, T, 1)
+            from oracle.evaluator import evaluate
+            ev = evaluate(W, T, osc)
+            win, _met = select_oracle(ev)
+            t1 = time.perf_counter() - t0
+            cpu = {"value": len(W) / t1, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
+                   "sample": "all %d standardized candidates (oracle/search.py graphs + oracle/evaluator.py) in "
+                             "%.2f s" % (len(W), t1)}
+            _C0.update(W=W, T=T, sc=osc)
+            t0 = time.perf_counter()
+            W2 = oracle_graphs(DEFAULT_TOPOLOGY, T, 1)
+            _C0["W"] = W2
+            cuts = np.linspace(0, len(W2), cores + 1).astype(int)
+            _pool_map(_c0_eval, list(zip(cuts[:-1], cuts[1:])), cores)
+            t2 = time.perf_counter() - t0
+            cpu_all = {"value": len(W2) / t2, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+                       "sample": "all %d candidates: graphs built once, scored in %d process shards, %.2f s"
+                                 % (len(W2), cores, t2)}
+            g = res[-1][1]
+            u64 = lambda x: np.float64(x).view(np.uint64)
+            parity = {"candidates": int(len(W)), "winner_index_equal": int(g["index"]) == win,
+                      "winner_f_h_p95_bits_equal": bool(u64(g["f"]) == u64(ev.f[win]) and u64(g["h"]) == u64(ev.h[win])
+                                                        and u64(g["p95_ms"]) == u64(ev.L[win])),
+                      "valid_count_equal": int(g["valid_count"]) == len(W)}
+            parity["bit_exact"] = all(v for k, v in parity.items() if k != "candidates")
+            wsample = _walk_stats(W[:: max(1, len(W) // 20000)], T, osc)
     elif args.workload == "c3":
         from paper_2304_09781_b200.controller import run_trace, ControllerParams
         from paper_2304_09781_b200.objective import AnnealParams
@@ -542,8 +661,17 @@ def run_other(args, rank, world, local):
         eng.build_feasibility(N_FLEET)
         tr = synthetic_trace(hours=24.0)
         ap = AnnealParams(proposal="uniform", evaluate="all", max_steps=args.max_steps)
+        # untimed warm-up re-plan of the same shape (module load, launch attributes, cluster size)
+        from paper_2304_09781_b200.search import anneal_chains, base_config
+        from paper_2304_09781_b200.graph import build_graph
+        w_base = np.array(build_graph(base_config(N_FLEET, prof), prof).weights, dtype=np.uint16)
+        anneal_chains(eng, np.repeat(w_base[None, :], args.chains, axis=0), prof,
+                      eng.calibrate(prof, N_FLEET, tr.mean(), LAMBDA, ci_base=tr.mean()), ap, SEED,
+                      chain_base=rank * args.chains)
+        t0 = time.perf_counter()
         rep = run_trace(eng, tr, "clover", N_FLEET, prof, LAMBDA, ap, ControllerParams(), seed=SEED,
                         chains=args.chains, chain_base=rank * args.chains)
+        t_trace = time.perf_counter() - t0
         res = [(r.device_ms, r.evals) for r in rep.replans]
         per_step = [e for _, e in res]
         cfg = "c3: 24 h synthetic ci trace (288 ticks at 5 min), re-plan when |dci|/ci > 5%% from the incumbent, " \
@@ -553,7 +681,15 @@ def run_other(args, rank, world, local):
         extra["replan_device_ms"] = json.dumps([round(r.device_ms, 3) for r in rep.replans])
         scaling = "weak"
         args.steps = len(res)
+        wall = sum(r.wall_ms for r in rep.replans) / 1000.0
+        E = prof.variant_count * 5
+        e2e = {"value": sum(per_step) / wall, "unit": UNIT, "h2d_bytes_per_step": args.chains * E * 2,
+               "d2h_bytes_per_step": args.chains * 80 + 2 * args.chains * E * 2 + 32,
+               "path": "controller.run_trace -> search.anneal_chains -> clv_replan per re-plan (host incumbent in, "
+                       "host winner out); wall time of the re-plans (%.2f s for the whole 24-h trace)" % t_trace}
         res = [(ms, None) for ms, _ in res]
+        if cpu_on:
+            cpu, cpu_all, parity, wsample = _c3_cpu(args, prof, tr, rep, cores)
     elif args.workload == "des":
         # SPEC serving-sim as the evaluator: one 10-minute DES per candidate fleet
         from paper_2304_09781_b200 import sim as S
@@ -580,6 +716,7 @@ def run_other(args, rank, world, local):
         extra["fleet_sims_per_s"] = str(C / (sum(r[0] for r in res) / 1000.0 / len(res)))
         scaling = "weak"
     elif args.workload == "c1":
+        from paper_2304_09781_b200.search import anneal_chains
         prof = synthetic_profile("efficientnet")
         n = 8
         eng.build_feasibility(n)
@@ -600,6 +737,41 @@ def run_other(args, rank, world, local):
         cfg = "c1: n=8 GPUs, EfficientNet B1-B7 (V=7), lambda sweep 0..1 (11 chains from BASE, one per lambda), " \
               "full GED<=4 neighbourhood per step, to termination; replicas across GPUs"
         scaling = "weak"
+        et, ee = [], 0
+        for s in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = anneal_chains(eng, start, prof, scs, ap, SEED + s, chain_base=rank * len(lams))
+            et.append(time.perf_counter() - t0)
+            if s >= args.warmup:
+                ee += r.evals
+        E = V * 5
+        e2e = {"value": ee / sum(et[args.warmup:]), "unit": UNIT, "h2d_bytes_per_step": len(lams) * E * 2,
+               "d2h_bytes_per_step": len(lams) * 80 + 2 * len(lams) * E * 2 + 32,
+               "path": "search.anneal_chains -> clv_replan (host starts in, host results out)"}
+        if cpu_on:
+            from oracle.tables import OracleTables
+            from oracle.evaluator import calibrate
+            from oracle.feasibility import FeasOracle
+            T = OracleTables.from_profile(prof)
+            _C0.update(T=T, scs=[calibrate(prof, T, n, 400.0, l) for l in lams], ap=ap,
+                       feas=FeasOracle(DEFAULT_TOPOLOGY, n))
+            jobs = [(start[i].astype(np.int64), i, SEED + args.warmup, args.max_steps) for i in range(len(lams))]
+            t0 = time.perf_counter()
+            outs1 = [_c1_chain(j) for j in jobs]
+            t1 = time.perf_counter() - t0
+            ev1 = sum(o.evals for o, _ in outs1)
+            cpu = {"value": ev1 / t1, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
+                   "sample": "the 11 lambda chains of the first timed step by oracle/anneal.py, %d candidates in "
+                             "%.2f s" % (ev1, t1), "replan_tts_s": t1}
+            t0 = time.perf_counter()
+            outsN = _pool_map(_c1_chain, jobs, min(cores, len(jobs)))
+            t2 = time.perf_counter() - t0
+            cpu_all = {"value": ev1 / t2, "unit": UNIT, "cores": min(cores, len(jobs)), "kind": "port",
+                       "cpu_model": cpu_model(), "sample": "same 11 chains, one process per chain",
+                       "replan_tts_s": t2}
+            parity = chain_parity([o for o, _ in outs1], res[0][1])
+            wsample = _chain_walk_stats([o for o, _ in outs1], T, _C0["scs"][5], n)
     else:
         pr, pb = synthetic_profile("resnet"), synthetic_profile("bert")
         sr, sb = eng.calibrate(pr, 128, 300.0, 0.5), eng.calibrate(pb, 128, 300.0, 0.5)
@@ -610,6 +782,17 @@ def run_other(args, rank, world, local):
         cfg = "c4: n=256 GPUs as two 128-GPU pods (ResNet V=5 | BERT V=6), counter-RNG x-space sweep of %d " \
               "candidates per step (sharded by index range)" % args.sweep
         scaling = "strong"
+        et = []
+        for s in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            eng.sweep(pods, b, e, SEED + s)
+            et.append(time.perf_counter() - t0)
+        e2e = {"value": (e - b) / (sum(et[args.warmup:]) / args.steps), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * ctypes.sizeof(NAT.EvalParams), "d2h_bytes_per_step": ctypes.sizeof(NAT.Best),
+               "path": "engine.sweep -> clv_sweep (host pod parameters in, winner record out)"}
+        if cpu_on:
+            cpu, cpu_all, parity, wsample = _c4_cpu(args, eng, pods, pr, pb, sr, sb, cores)
     ms = [r[0] for r in res]
     t = torch.tensor([sum(ms) / 1000.0, float(sum(per_step))], dtype=torch.float64,
                      device="cuda" if os.environ.get("CLV_DIST_BACKEND", "nccl") == "nccl" else "cpu")
@@ -619,14 +802,143 @@ def run_other(args, rank, world, local):
         t = torch.cat([a, c])
     if rank == 0:
         unit = extra.pop("_unit", UNIT)
+        kernel = {"c0": "clv::oracle_kernel", "c1": "clv::anneal_kernel", "c3": "clv::anneal_kernel",
+                  "c4": "clv::sweep_kernel"}.get(args.workload)
+        if kernel:
+            launch_s = t[0].item() / args.steps
+            cand = t[1].item() / args.steps
+            note = {"c4": "two pods per candidate: the E_nz / K of both pods' graphs summed, plus ~1064 integer "
+                          "draws per candidate not counted",
+                    "c1": "anneal_kernel with the exact screen (DESIGN.md): most candidates get only A, E, f",
+                    "c3": "anneal_kernel with the exact screen (DESIGN.md): most candidates get only A, E, f",
+                    "c0": "standardized graphs decoded from the index"}[args.workload]
+            roof = _fp64_roofline(cand, launch_s, *(wsample or (None, None)), kernel, note)
         line = {"metric": METRIC, "value": t[1].item() / t[0].item(), "unit": unit, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t[0].item() / args.steps,
                 "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": {"workload": cfg}, "candidates_per_step": t[1].item() / args.steps}
-        line.update({k: str(v) for k, v in extra.items()})
+        if e2e is not None:
+            line["e2e"] = e2e
+        if roof is not None:
+            line["roofline"] = roof
+        line["cpu_baseline"] = cpu
+        if cpu_all is not None:
+            line["cpu_all_cores"] = cpu_all
+        if parity is not None:
+            line["parity"] = parity
+        line.update({k: (v if isinstance(v, (int, float, dict, list)) else str(v)) for k, v in extra.items()})
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _chain_walk_stats(outs, T, sc, n):
+    """E_nz / walk length over the neighbourhoods of the chains' start graphs (oracle sample)."""
+    from oracle.neighbours import enumerate_neighbours
+    from oracle.feasibility import FeasOracle
+    from paper_2304_09781_b200.mig import DEFAULT_TOPOLOGY
+    feas = FeasOracle(DEFAULT_TOPOLOGY, n)
+    Ws = [enumerate_neighbours(o.best_w, T.mem_ok, T.V, n, feas).W for o in outs[:4]]
+    Ws = [w for w in Ws if len(w)]
+    return _walk_stats(np.concatenate(Ws), T, sc) if Ws else (None, None)
+
+
+def _c3_cpu(args, prof, tr, rep, cores):
+    """CPU oracle controller (oracle/controller.py) over the trace up to the GPU run's third
+    re-plan: all host cores (one chain per process), per-re-plan time-to-solution, and the
+    incumbent of every tick compared with the GPU timeline; one core on one chain."""
+    from oracle.tables import OracleTables
+    from oracle.feasibility import FeasOracle
+    from oracle.controller import run_trace_clover, _chain_job
+    from oracle.evaluator import calibrate
+    from paper_2304_09781_b200.mig import DEFAULT_TOPOLOGY
+    from paper_2304_09781_b200.objective import AnnealParams
+    import multiprocessing as mp
+    T = OracleTables.from_profile(prof)
+    feas = FeasOracle(DEFAULT_TOPOLOGY, N_FLEET)
+    ap = AnnealParams(proposal="uniform", evaluate="all", max_steps=args.max_steps)
+    samples = list(tr.samples)
+    nrep = min(3, len(rep.replans))
+    last_tick = rep.replans[nrep - 1].tick
+    def fork_map(fn, jobs):                      # jobs travel by fork, not by pickling (ctypes handles)
+        _C0.update(fn=fn, jobs=jobs)
+        with mp.get_context("fork").Pool(cores) as pool:
+            return pool.map(_c3_job, range(len(jobs)), chunksize=1)
+    t0 = time.perf_counter()
+    rows = run_trace_clover(samples, N_FLEET, prof, T, LAMBDA, ap, SEED, args.chains, feas, map_fn=fork_map,
+                            ticks=last_tick + 1)
+    wall = time.perf_counter() - t0
+    gpu_rows = rep.rows[:len(rows)]
+    g_rep = [r for r in rep.replans if r.tick < len(rows)]
+    same = (len(gpu_rows) == len(rows)
+            and [r.tick for r in g_rep] == [x["tick"] for x in rows if x["replanned"]]
+            and [r.accepted for r in g_rep] == [x["accepted"] for x in rows if x["replanned"]]
+            and all(g["sla_met"] == x["sla"] and g["accuracy"] == x["accuracy"] for g, x in zip(gpu_rows, rows))
+            and gpu_rows[-1]["cumulative_gco2"] == rows[-1]["cum"])
+    evals = sum(r.evals for r in rep.replans[:nrep])
+    cpu_all = {"value": evals / wall, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+               "sample": "oracle/controller.py over the first %d ticks (%d re-plans x %d chains, one chain per "
+                         "process)" % (len(rows), nrep, args.chains),
+               "replan_tts_s_mean": wall / nrep}
+    # one core: the first re-plan's first chain
+    ci0 = samples[0][1]
+    ci_mean = sum(c for _, c in samples) / len(samples)
+    sc = calibrate(prof, T, N_FLEET, ci_mean, LAMBDA, ci_base=ci_mean).with_ci(ci0)
+    from oracle.evaluator import base_graph
+    from oracle.rng import derive_seed
+    t0 = time.perf_counter()
+    out = _chain_job((base_graph(T.V, N_FLEET), N_FLEET, T, sc, ap, derive_seed(SEED, 0), 0, feas))
+    t1 = time.perf_counter() - t0
+    cpu = {"value": out.evals / t1, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
+           "sample": "chain 0 of the first re-plan (oracle/anneal.py), %d candidates in %.2f s" % (out.evals, t1)}
+    parity = {"ticks_compared": len(rows), "replans": nrep, "bit_exact": bool(same),
+              "compared": "re-plan ticks, accepted flags, per-tick SLA flag and accuracy bits, cumulative gCO2 bits "
+                          "of the GPU controller vs oracle/controller.py"}
+    wsample = _chain_walk_stats([out], T, sc, N_FLEET)
+    return cpu, cpu_all, parity, wsample
+
+
+def _c4_cpu(args, eng, pods, pr, pb, sr, sb, cores):
+    """CPU oracle sweep (oracle/search.py) on a prefix of the same counter-RNG stream: one core on
+    2,000 candidates, all cores on 100,000; parity = f, h, SLA bits of the 100,000 and the winner."""
+    from oracle.tables import OracleTables
+    from oracle.evaluator import calibrate
+    from oracle.search import Pod, select_best, draw_candidate, fleet_graph
+    from paper_2304_09781_b200.mig import DEFAULT_TOPOLOGY
+    Tr, Tb = OracleTables.from_profile(pr), OracleTables.from_profile(pb)
+    opods = [Pod(Tr, calibrate(pr, Tr, 128, 300.0, 0.5), 128, 0.5), Pod(Tb, calibrate(pb, Tb, 128, 300.0, 0.5), 128, 0.5)]
+    seed = SEED + args.warmup
+    _C0.update(seed=seed, pods=opods, topo=DEFAULT_TOPOLOGY)
+    n1, nall = 2000, 100_000
+    t0 = time.perf_counter()
+    _c4_eval((0, n1))
+    t1 = time.perf_counter() - t0
+    cpu = {"value": n1 / t1, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
+           "sample": "candidates [0, %d) of the first timed step's stream (oracle/search.py)" % n1}
+    cuts = np.linspace(0, nall, cores * 4 + 1).astype(int)
+    t0 = time.perf_counter()
+    parts = _pool_map(_c4_eval, list(zip(cuts[:-1], cuts[1:])), cores)
+    t2 = time.perf_counter() - t0
+    f = np.concatenate([p[0] for p in parts]); h = np.concatenate([p[1] for p in parts])
+    sla = np.concatenate([p[2] for p in parts])
+    cpu_all = {"value": nall / t2, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+               "sample": "candidates [0, %d) in %d process shards" % (nall, len(cuts) - 1)}
+    best, outs = eng.sweep(pods, 0, nall, seed, outputs=True)
+    gf, gh = outs["f"].cpu().numpy(), outs["h"].cpu().numpy()
+    gs = outs["sla"].cpu().numpy().astype(bool)
+    win = select_best(h, sla)
+    parity = {"candidates": nall, "f_bits_equal": bool(np.array_equal(gf.view(np.uint64), f.view(np.uint64))),
+              "h_bits_equal": bool(np.array_equal(gh.view(np.uint64), h.view(np.uint64))),
+              "sla_equal": bool(np.array_equal(gs, sla)), "winner_index_equal": int(best["index"]) == win}
+    parity["bit_exact"] = all(v for k, v in parity.items() if k != "candidates")
+    # work model: both pods' graphs of a 500-candidate sample
+    Wr, Wb = [], []
+    for i in range(500):
+        (pp, aa), (pq, ab) = draw_candidate(seed, i, opods, DEFAULT_TOPOLOGY)
+        Wr.append(fleet_graph(pp, aa, DEFAULT_TOPOLOGY, Tr)); Wb.append(fleet_graph(pq, ab, DEFAULT_TOPOLOGY, Tb))
+    er, kr = _walk_stats(np.array(Wr), Tr, opods[0].scenario)
+    eb, kb = _walk_stats(np.array(Wb), Tb, opods[1].scenario)
+    return cpu, cpu_all, parity, (er + eb, kr + kb + 73.0 / 7.0)
 
 
 if __name__ == "__main__":

@@ -35,8 +35,9 @@ def intensity_at(samples, t):
 
 
 def run_trace_clover(samples, n, profile, tables, lam, ap, seed, chains, feas, step_s=300.0, threshold=0.05,
-                     utilization=0.7, pue=1.5, map_fn=None, chain_base=0):
-    """map_fn(fn, args) runs a re-plan's independent chains, e.g. a process pool's map."""
+                     utilization=0.7, pue=1.5, map_fn=None, chain_base=0, ticks=None):
+    """map_fn(fn, args) runs a re-plan's independent chains (SPEC:485), e.g. a process pool's map;
+    ticks stops after that many ticks (a prefix of the same run)."""
     ci_mean = sum(c for _, c in samples) / len(samples)
     base_sc = calibrate(profile, tables, n, ci_mean, lam, utilization, ci_base=ci_mean, pue=pue)
     V = tables.V
@@ -46,6 +47,8 @@ def run_trace_clover(samples, n, profile, tables, lam, ap, seed, chains, feas, s
     cum = 0.0
     out = []
     steps = int(round((samples[-1][0] - samples[0][0]) / step_s)) + 1
+    if ticks is not None:
+        steps = min(steps, int(ticks))
     for tick in range(steps):
         t = samples[0][0] + tick * step_s
         ci = intensity_at(samples, t)

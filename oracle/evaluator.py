@@ -114,6 +114,32 @@ def p95_walk(W: np.ndarray, tables: OracleTables, W0: np.ndarray, c20: float) ->
     return lq
 
 
+def walk_lengths(W: np.ndarray, tables: OracleTables, scenario) -> np.ndarray:
+    """Ranks visited by each fleet's p95 walk (the K of the per-candidate work model in
+    DESIGN.md; measurement only, not part of the evaluator)."""
+    s_thr, s_acc, s_en, s_idle, (Wm, s2, s3), m = aggregates(W, tables)
+    c = constants(tables, scenario)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = 1.0 / s_thr.astype(np.float64)
+        rho_c = np.minimum(c["R_q"] * inv, 1.0)
+        W0 = idle_wait_ms(np.asarray(m, dtype=np.float64), s_thr.astype(np.float64), np.asarray(s2, dtype=np.float64),
+                          np.asarray(s3, dtype=np.float64), c["R"], c["R_q"], inv, rho_c, tables)
+    n = len(Wm)
+    P, Q = np.zeros(n), np.ones(n)
+    done = np.zeros(n, dtype=bool)
+    K = np.zeros(n, dtype=np.int64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        for e in reversed(rank_order(tables)):
+            act = ~done & (Wm[:, e] > 0)
+            d = float(tables.mean_ms[e]) + W0
+            Pn = P * d + (Wm[:, e].astype(np.float64) * c["c20"]) * Q
+            P = np.where(act, Pn, P)
+            Q = np.where(act, Q * d, Q)
+            K += act
+            done = done | (act & (P > Q))
+    return K
+
+
 def aggregates(W: np.ndarray, tables: OracleTables):
     W = np.asarray(W, dtype=np.int64).reshape(-1, tables.E)
     s_thr = W @ tables.thr_q

@@ -1,13 +1,16 @@
 #!/bin/bash
-# Run on the GPU box: every bench workload + the reference arm; one JSON line each in gpurun_out/all_*.json
+# Run on the GPU box: every bench workload + the reference arm; one JSON line each in gpurun_out/${TAG}_*.json
+TAG=${TAG:-all}
 mkdir -p gpurun_out
 python -m paper_2304_09781_b200.build > /dev/null
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/all_c2.json 2> gpurun_out/all_c2.err
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/all_ref.json 2> gpurun_out/all_ref.err
-for w in c0 c1 c4 des; do
-  timeout 900 python bench.py --workload $w --steps 5 --warmup 3 > gpurun_out/all_$w.json 2> gpurun_out/all_$w.err
+nproc > gpurun_out/${TAG}_nproc.txt; lscpu | grep "Model name" >> gpurun_out/${TAG}_nproc.txt
+for w in ${WORKLOADS:-c0 c1 c4 c3}; do
+  if [ $w = c3 ]; then A="--steps 1 --warmup 0"; else A="--steps 5 --warmup 3"; fi
+  timeout 1200 python bench.py --workload $w $A > gpurun_out/${TAG}_$w.json 2> gpurun_out/${TAG}_$w.err
 done
-timeout 900 python bench.py --workload c3 --steps 1 --warmup 0 > gpurun_out/all_c3.json 2> gpurun_out/all_c3.err
-timeout 600 python tools/bench_kernels.py > gpurun_out/all_kernels.json 2> gpurun_out/all_kernels.err
-nproc > gpurun_out/nproc.txt; lscpu | grep "Model name" >> gpurun_out/nproc.txt
-for f in gpurun_out/all_*.json; do echo "== $f"; tail -c 600 $f; echo; done
+if [ -n "$WITH_C2" ]; then
+  timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/${TAG}_c2.json 2> gpurun_out/${TAG}_c2.err
+  timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err
+fi
+for f in gpurun_out/${TAG}_*.json; do echo "== $f"; tail -c 1500 $f; echo; done
+for f in gpurun_out/${TAG}_*.err; do echo "== $f"; tail -5 $f; done
