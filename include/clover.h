@@ -11,6 +11,12 @@
  * the cudaStream_t passed as `stream` (NULL = legacy default stream); calls
  * that fill a host-side clv_best synchronise that stream.
  *
+ * A context is NOT re-entrant across streams: its scratch (selection partials,
+ * the chain move log, the re-plan staging buffers, the DES workload cache) is
+ * shared by every call, so all calls on one context must be issued from ONE
+ * stream at a time (or be ordered by the caller with events).  Use one context
+ * per concurrent stream.  ("not re-entrant, stream-ordered".)
+ *
  * Reference interface each entry point replaces (SPEC = reference SPEC.md,
  * mig.py / core.py = reference pkg/src/carbon_sched/):
  *   clv_set_topology        MigTopology.__init__ / load_topology      mig.py:94-123, 201-217
@@ -39,7 +45,7 @@
 extern "C" {
 #endif
 
-#define CLV_ABI_VERSION 2
+#define CLV_ABI_VERSION 3
 #define CLV_MAX_VARIANTS 8
 #define CLV_MAX_EDGES 40
 #define CLV_MAX_CONFIGS 32
@@ -100,7 +106,13 @@ typedef struct clv_anneal_params {
     int32_t max_steps;
     int32_t proposal;        /* 0 = best-h neighbour, 1 = uniform (min-hash) neighbour */
     int32_t evaluate;        /* 0 = score whole neighbourhood, 1 = score proposal only */
+    int32_t flags;           /* CLV_ANNEAL_MULT_COOLING | CLV_ANNEAL_PAPER_MOVES (0 = SPEC defaults) */
 } clv_anneal_params;
+
+/* clv_anneal_params.flags */
+#define CLV_ANNEAL_MULT_COOLING 1  /* T_k = max(t_floor, t_init (1 - cooling_step)^k), SPEC:492 option */
+#define CLV_ANNEAL_PAPER_MOVES  2  /* + one-instance add / remove moves (GED 1):
+                                      indices E*E + NP*NP + a (add on edge a), + E + r (remove from r) */
 
 /* Per-chain result written by clv_anneal (device memory). */
 typedef struct clv_chain_result {

@@ -2,7 +2,8 @@
 
 One chain, sequential by definition.  Step semantics follow
 DESIGN.md "Chain step": temperature T_k = max(t_floor,
-t_init - k*cooling); best tracking SLA-first then lowest h,
+t_init - k*cooling) (or t_init (1 - cooling)^k, SPEC:492's multiplicative
+option); move set SPEC (default) or paper (+ unit add/remove); best tracking SLA-first then lowest h,
 ties keep the incumbent; stall after ``stall_limit``
 steps without a new best; Eq. 7 acceptance with
 u = uniform01(derive_seed(seed, chain, k, 0)).
@@ -45,9 +46,16 @@ def anneal_chain(w0, n, tables, scenario, ap, seed, chain, feas, log=False) -> C
     best, best_w, best_step, best_idx = dict(cur), w.copy(), -1, -1
     evals, stall, status, steps = 1, 0, MAX_STEPS, 0
     rows = []
+    moves = getattr(ap, "move_set", "spec")
+    mult = getattr(ap, "cooling", "subtractive") == "multiplicative"
+    t_raw, factor = ap.t_init, 1.0 - ap.cooling_step
     for k in range(ap.step_limit()):
-        T = max(ap.t_floor, ap.t_init - k * ap.cooling_step)
-        nb = enumerate_neighbours(w, tables.mem_ok, V, n, feas)
+        if mult:                                 # T_k = max(t_floor, t_init (1 - cooling)^k), iterated
+            T = max(ap.t_floor, t_raw)
+            t_raw = t_raw * factor
+        else:
+            T = max(ap.t_floor, ap.t_init - k * ap.cooling_step)
+        nb = enumerate_neighbours(w, tables.mem_ok, V, n, feas, moves)
         if len(nb) == 0:
             status = NO_NEIGHBOR
             break
@@ -79,7 +87,7 @@ def anneal_chain(w0, n, tables, scenario, ap, seed, chain, feas, log=False) -> C
         hp, hc = prop["h"], cur["h"]
         accept = hp <= hc or u < exp_clv(-(hp - hc) / T)
         if log:
-            rows.append(dict(iter=k, temp=T, ged_from_center=2 * int(nb.kind[p]), n_neighbours=len(nb), f=prop["f"],
+            rows.append(dict(iter=k, temp=T, ged_from_center=int(nb.ged[p]), n_neighbours=len(nb), f=prop["f"],
                              h=prop["h"], p95_ms=prop["L"], sla_met=prop["sla"],
                              accepted=bool(accept), new_best=bool(new_best)))
         if accept:

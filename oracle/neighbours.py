@@ -10,6 +10,12 @@ the resulting slice multiset realizable on n GPUs.  Canonical index:
   double  ({r1<=r2}, {a1<=a2}) -> E*E + P(r1, r2) * NP + P(a1, a2)
 with P the row-major index of a sorted pair and NP = E(E+1)/2.  The device
 enumerates the same set by a different (adjacency-driven) route.
+
+moves="paper" (every configuration within the GED threshold) adds
+the unit instance moves that change the instance count m:
+  add one instance on edge a    -> E*E + NP*NP + a        (GED 1; a memory-feasible)
+  remove one instance of edge r -> E*E + NP*NP + E + r    (GED 1; r present)
+each kept when the new slice multiset is realizable on n GPUs.
 """
 
 from __future__ import annotations
@@ -34,16 +40,17 @@ def adjacency(V: int) -> np.ndarray:
 
 
 class Neighbourhood:
-    __slots__ = ("idx", "W", "r1", "r2", "a1", "a2", "kind")
+    __slots__ = ("idx", "W", "r1", "r2", "a1", "a2", "kind", "ged")
 
-    def __init__(self, idx, W, r1, r2, a1, a2, kind):
+    def __init__(self, idx, W, r1, r2, a1, a2, kind, ged=None):
         self.idx, self.W, self.r1, self.r2, self.a1, self.a2, self.kind = idx, W, r1, r2, a1, a2, kind
+        self.ged = 2 * np.asarray(kind, dtype=np.int64) if ged is None else ged
 
     def __len__(self):
         return len(self.idx)
 
 
-def enumerate_neighbours(w, mem_ok, V: int, n: int, feas) -> Neighbourhood:
+def enumerate_neighbours(w, mem_ok, V: int, n: int, feas, moves: str = "spec") -> Neighbourhood:
     w = np.asarray(w, dtype=np.int64)
     E = V * 5
     NP = E * (E + 1) // 2
@@ -72,13 +79,21 @@ def enumerate_neighbours(w, mem_ok, V: int, n: int, feas) -> Neighbourhood:
     else:
         r1 = r2 = a1 = a2 = d_idx = np.zeros(0, dtype=np.int64)
     n1, n2 = len(r), len(r1)
-    Wn = np.repeat(w[None, :], n1 + n2, axis=0)
+    if moves == "paper":                         # unit add / remove (GED 1)
+        u_add, u_rem = okA, present
+    else:
+        u_add = u_rem = np.zeros(0, dtype=np.int64)
+    n3, n4 = len(u_add), len(u_rem)
+    Wn = np.repeat(w[None, :], n1 + n2 + n3 + n4, axis=0)
     rows1 = np.arange(n1)
     np.subtract.at(Wn, (rows1, r), 1)
     np.add.at(Wn, (rows1, a), 1)
     rows2 = n1 + np.arange(n2)
     for col, sign in ((r1, -1), (r2, -1), (a1, 1), (a2, 1)):
         np.add.at(Wn, (rows2, col), sign)
+    base = E * E + NP * NP
+    np.add.at(Wn, (n1 + n2 + np.arange(n3), u_add), 1)
+    np.add.at(Wn, (n1 + n2 + n3 + np.arange(n4), u_rem), -1)
     # fleet feasibility of the new slice multisets
     svec = Wn.reshape(len(Wn), V, 5).sum(axis=1)
     feas_ok = np.zeros(len(Wn), dtype=bool)
@@ -86,13 +101,15 @@ def enumerate_neighbours(w, mem_ok, V: int, n: int, feas) -> Neighbourhood:
         uniq, inv = np.unique(svec, axis=0, return_inverse=True)
         okv = feas.feasible_batch(uniq, n)
         feas_ok = okv[inv.reshape(-1)]
-    idx = np.concatenate([s_idx, d_idx])
-    R1 = np.concatenate([r, r1]); R2 = np.concatenate([np.full(n1, -1), r2])
-    A1 = np.concatenate([a, a1]); A2 = np.concatenate([np.full(n1, -1), a2])
-    kind = np.concatenate([np.ones(n1, dtype=np.int8), np.full(n2, 2, dtype=np.int8)])
+    none3, none4 = np.full(n3, -1), np.full(n4, -1)
+    idx = np.concatenate([s_idx, d_idx, base + u_add, base + E + u_rem])
+    R1 = np.concatenate([r, r1, none3, u_rem]); R2 = np.concatenate([np.full(n1, -1), r2, none3, none4])
+    A1 = np.concatenate([a, a1, u_add, none4]); A2 = np.concatenate([np.full(n1, -1), a2, none3, none4])
+    kind = np.concatenate([np.ones(n1, dtype=np.int8), np.full(n2, 2, dtype=np.int8), np.zeros(n3 + n4, dtype=np.int8)])
+    ged = np.concatenate([np.full(n1, 2), np.full(n2, 4), np.ones(n3 + n4, dtype=np.int64)]).astype(np.int64)
     sel = np.nonzero(feas_ok)[0]
     order = sel[np.argsort(idx[sel], kind="stable")]
-    return Neighbourhood(idx[order], Wn[order], R1[order], R2[order], A1[order], A2[order], kind[order])
+    return Neighbourhood(idx[order], Wn[order], R1[order], R2[order], A1[order], A2[order], kind[order], ged[order])
 
 
 def brute_force_neighbours(w, mem_ok, V: int, n: int, feas) -> set:

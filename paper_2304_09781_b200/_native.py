@@ -35,7 +35,8 @@ class Best(ctypes.Structure):
 
 class AnnealParamsC(ctypes.Structure):
     _fields_ = [("t_init", c_f64), ("cooling_step", c_f64), ("t_floor", c_f64),
-                ("stall_limit", c_i32), ("max_steps", c_i32), ("proposal", c_i32), ("evaluate", c_i32)]
+                ("stall_limit", c_i32), ("max_steps", c_i32), ("proposal", c_i32), ("evaluate", c_i32),
+                ("flags", c_i32)]
 
 
 class ChainResult(ctypes.Structure):
@@ -126,7 +127,7 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.clv_abi_version() != 2:
+    if lib.clv_abi_version() != 3:
         raise E.DeviceError("ABI version mismatch")
     _lib = lib
     return lib

@@ -55,7 +55,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             errors.append(out)
     if errors:
         raise RuntimeError("nvcc failed:\n" + "\n".join(errors))
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp"] + [o for o, _ in jobs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp"] + [o for o, _ in jobs] \
+        + ["-ldl"]   # NVTX3 (header-only) loads an injection library only when a tool is attached
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)

@@ -185,12 +185,13 @@ def run_trace(engine: CloverEngine, trace: CarbonTrace, scheme: str, n: int, pro
                 cand = dict(f=o["f"], h=o["h"], p95_ms=o["p95_ms"], sla_met=bool(o["sla_met"]))
                 evals = o["valid_count"]
             else:
-                budget = max(1, math.ceil(ap.time_budget_s / ap.eval_cost_s))
-                best, _ = engine.sweep([(profile, sc, n, 1.0)], 0, budget, tick_seed)
-                fc = engine.sweep_decode([(profile, sc, n, 1.0)], tick_seed, best["index"])[0]
+                # the same termination rules as the anneal re-plan (SPEC acceptance 7): draws
+                # bounded by max_steps + 1 and the time budget, stall_limit without a new best
+                from .search import blover_run
+                fc, best, blog = blover_run(engine, profile, sc, n, ap, tick_seed)
                 cand_w = np.array(build_graph(fc, profile).weights, dtype=np.int64)
-                cand = dict(f=best["f"], h=best["h"], p95_ms=0.0, sla_met=bool(best["sla_met"]))
-                evals = best["valid_count"]
+                cand = dict(f=best["f"], h=best["h"], p95_ms=best["p95_ms"], sla_met=bool(best["sla_met"]))
+                evals = len(blog)
             e1.record()
             torch.cuda.synchronize()
             dev_ms = e0.elapsed_time(e1)

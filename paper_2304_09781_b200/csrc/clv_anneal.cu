@@ -114,6 +114,8 @@ struct __align__(16) AnnealSmem {
     EvalConst ec;
     unsigned long long mem_ok;
     unsigned magicE, magicNP;              // ceil(2^32 / E), ceil(2^32 / NP) (exact small divisions)
+    unsigned ubase;                        // E*E + NP*NP: first paper (unit) move index
+    int ub_dirty;                          // a unit move changed m: ub[] needs the new W0 bound
     unsigned char sl[CLV_MAX_EDGES];       // slice kind of the edge
     unsigned short pair_tab[MAXP];         // P -> (x | y << 8)
     unsigned char pair_len[MAXP];          // static move-list lengths (staged from FamilyTables)
@@ -144,6 +146,7 @@ struct __align__(16) AnnealSmem {
     int fsvec[CLV_K];                      // slice vector the feasibility bytes belong to
     unsigned char feasS[25];
     unsigned char feasD[625];
+    unsigned char feasAR[10];              // paper moves: slice vector + e_k (0..4), - e_k (5..9) realizable
     // reductions
     KRec wS[NWARP], wV[NWARP], wP[NWARP];
     unsigned long long wc[NWARP];
@@ -185,6 +188,12 @@ struct GraphWalk {
 __device__ inline void decode_move(const AnnealSmem &s, int E, long long idx64, int &r1, int &r2, int &a1, int &a2) {
     // divisions by E and NP as multiply-high by ceil(2^32 / d): exact because n * d < 2^32
     const unsigned idx = (unsigned)idx64;
+    if (idx >= s.ubase) {                                    // paper moves: add a, remove r
+        const int u = (int)(idx - s.ubase);
+        r2 = 0xFF; a2 = 0xFF;
+        if (u < E) { r1 = 0xFF; a1 = u; } else { r1 = u - E; a1 = 0xFF; }
+        return;
+    }
     if (idx < (unsigned)(E * E)) {
         r1 = (int)__umulhi(idx, s.magicE); a1 = (int)(idx - (unsigned)r1 * E); r2 = 0xFF; a2 = 0xFF;
         return;
@@ -217,7 +226,8 @@ __device__ inline Score score_move(const AnnealSmem &s, int r1, int r2, int a1, 
     }
     CandWalk cw{&s, m, r1 == 0xFF ? 0xFF : s.rk[r1], r2 == 0xFF ? 0xFF : s.rk[r2],
                 a1 == 0xFF ? 0xFF : s.rk[a1], a2 == 0xFF ? 0xFF : s.rk[a2]};
-    return epilogue_d(t, ac, en, id, q2, q3, s.mcount, s.ec, cw);
+    const double mc = s.mcount + (double)((a1 != 0xFF) + (a2 != 0xFF) - (r1 != 0xFF) - (r2 != 0xFF));
+    return epilogue_d(t, ac, en, id, q2, q3, mc, s.ec, cw);
 }
 
 // Apply a move to a bare weight vector (best-graph reconstruction).
@@ -230,43 +240,61 @@ __device__ inline void move_graph(const AnnealSmem &s, int E, long long idx, int
     if (a2 != 0xFF) w[a2] += 1;
 }
 
-// Apply a move to the CTA-local centre (thread 0) -- O(1).
+// Apply a move to the CTA-local centre (thread 0) -- O(1).  Absent edges (0xFF) act as
+// zero rows: S + ((A1 + A2) - (R1 + R2)) is the edge-by-edge update bit for bit (exact
+// integers).  Unit add / remove moves (paper move set) change the instance count m.
 __device__ inline void apply_move(AnnealSmem &s, int E, long long idx) {
-    // All loads first, one update per field: the centre sums are exact integers, so
-    // S + ((A1 + A2) - (R1 + R2)) equals the edge-by-edge update bit for bit.
     int r1, r2, a1, a2;
     decode_move(s, E, idx, r1, r2, a1, a2);
-    const bool two = r2 != 0xFF;                   // a double move has r2 and a2
-    const ARow R1 = s.row[r1], A1 = s.row[a1];
-    ARow R2 = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, A2 = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int wr2 = 0, wa2 = 0;
-    if (two) { R2 = s.row[r2]; A2 = s.row[a2]; wr2 = s.w[r2]; wa2 = s.w[a2]; }
-    const int wr1 = s.w[r1], wa1 = s.w[a1];
-    unsigned long long m = s.pmask;
-    const unsigned long long br1 = s.rbit[r1], ba1 = s.rbit[a1];
-    const unsigned long long br2 = two ? s.rbit[r2] : 0ULL, ba2 = two ? s.rbit[a2] : 0ULL;
-    s.S[0] = s.S[0] + ((A1.thr + A2.thr) - (R1.thr + R2.thr));
-    s.S[1] = s.S[1] + ((A1.acc + A2.acc) - (R1.acc + R2.acc));
-    s.S[2] = s.S[2] + ((A1.en + A2.en) - (R1.en + R2.en));
-    s.S[3] = s.S[3] + ((A1.idle + A2.idle) - (R1.idle + R2.idle));
-    s.S[4] = s.S[4] + ((A1.t2 + A2.t2) - (R1.t2 + R2.t2));
-    s.S[5] = s.S[5] + ((A1.t3 + A2.t3) - (R1.t3 + R2.t3));
-    const int nr1 = wr1 - 1 - ((two && r2 == r1) ? 1 : 0);
-    const int nr2 = two ? ((r2 == r1) ? nr1 : wr2 - 1) : 1;
-    const int na1 = wa1 + 1 + ((two && a2 == a1) ? 1 : 0);
-    s.w[r1] = nr1;
-    s.w[a1] = na1;
-    if (two) { s.w[r2] = nr2; s.w[a2] = (a2 == a1) ? na1 : wa2 + 1; }
-    s.wr[s.rk[r1]] = (double)s.w[r1];
-    s.wr[s.rk[a1]] = (double)s.w[a1];
-    if (two) { s.wr[s.rk[r2]] = (double)s.w[r2]; s.wr[s.rk[a2]] = (double)s.w[a2]; }
-    const int kr1 = r1 % CLV_K, ka1 = a1 % CLV_K, kr2 = two ? r2 % CLV_K : -1, ka2 = two ? a2 % CLV_K : -1;
+    if (r1 != 0xFF && a1 != 0xFF) {
+        // SPEC move (m unchanged): all loads first, one update per field
+        const bool two = r2 != 0xFF;                   // a double move has r2 and a2
+        const ARow R1 = s.row[r1], A1 = s.row[a1];
+        ARow R2 = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, A2 = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        int wr2 = 0, wa2 = 0;
+        if (two) { R2 = s.row[r2]; A2 = s.row[a2]; wr2 = s.w[r2]; wa2 = s.w[a2]; }
+        const int wr1 = s.w[r1], wa1 = s.w[a1];
+        unsigned long long m = s.pmask;
+        const unsigned long long br1 = s.rbit[r1], ba1 = s.rbit[a1];
+        const unsigned long long br2 = two ? s.rbit[r2] : 0ULL, ba2 = two ? s.rbit[a2] : 0ULL;
+        s.S[0] = s.S[0] + ((A1.thr + A2.thr) - (R1.thr + R2.thr));
+        s.S[1] = s.S[1] + ((A1.acc + A2.acc) - (R1.acc + R2.acc));
+        s.S[2] = s.S[2] + ((A1.en + A2.en) - (R1.en + R2.en));
+        s.S[3] = s.S[3] + ((A1.idle + A2.idle) - (R1.idle + R2.idle));
+        s.S[4] = s.S[4] + ((A1.t2 + A2.t2) - (R1.t2 + R2.t2));
+        s.S[5] = s.S[5] + ((A1.t3 + A2.t3) - (R1.t3 + R2.t3));
+        const int nr1 = wr1 - 1 - ((two && r2 == r1) ? 1 : 0);
+        const int nr2 = two ? ((r2 == r1) ? nr1 : wr2 - 1) : 1;
+        const int na1 = wa1 + 1 + ((two && a2 == a1) ? 1 : 0);
+        s.w[r1] = nr1;
+        s.w[a1] = na1;
+        if (two) { s.w[r2] = nr2; s.w[a2] = (a2 == a1) ? na1 : wa2 + 1; }
+        s.wr[s.rk[r1]] = (double)s.w[r1];
+        s.wr[s.rk[a1]] = (double)s.w[a1];
+        if (two) { s.wr[s.rk[r2]] = (double)s.w[r2]; s.wr[s.rk[a2]] = (double)s.w[a2]; }
+        const int kr1 = r1 % CLV_K, ka1 = a1 % CLV_K, kr2 = two ? r2 % CLV_K : -1, ka2 = two ? a2 % CLV_K : -1;
 #pragma unroll
-    for (int k = 0; k < CLV_K; ++k)
-        s.svec[k] += (k == ka1) + (k == ka2) - (k == kr1) - (k == kr2);
-    if (nr1 == 0) m &= ~br1;
-    if (nr2 == 0) m &= ~br2;
-    s.pmask = m | ba1 | ba2;
+        for (int k = 0; k < CLV_K; ++k)
+            s.svec[k] += (k == ka1) + (k == ka2) - (k == kr1) - (k == kr2);
+        if (nr1 == 0) m &= ~br1;
+        if (nr2 == 0) m &= ~br2;
+        s.pmask = m | ba1 | ba2;
+        return;
+    }
+    // paper unit move: one instance added on a1 or removed from r1 (m changes)
+    const bool add = a1 != 0xFF;
+    const int e = add ? a1 : r1;
+    const ARow A = s.row[e];
+    const double sg = add ? 1.0 : -1.0;
+    s.S[0] = s.S[0] + sg * A.thr; s.S[1] = s.S[1] + sg * A.acc; s.S[2] = s.S[2] + sg * A.en;
+    s.S[3] = s.S[3] + sg * A.idle; s.S[4] = s.S[4] + sg * A.t2; s.S[5] = s.S[5] + sg * A.t3;
+    const int nw = s.w[e] + (add ? 1 : -1);
+    s.w[e] = nw;
+    s.wr[s.rk[e]] = (double)nw;
+    s.svec[e % CLV_K] += add ? 1 : -1;
+    s.pmask = nw > 0 ? (s.pmask | s.rbit[e]) : (s.pmask & ~s.rbit[e]);
+    s.mcount += sg;
+    s.ub_dirty = 1;
 }
 
 __device__ __forceinline__ void pen_factors(double lb, double slo, float &pu, float &pl);
@@ -310,7 +338,7 @@ __device__ __forceinline__ void pen_factors(double lb, double slo, float &pu, fl
 // the move space by table position), the present-edge entries, and -- only when
 // the centre's slice multiset changed -- the feasibility bytes of all 25 single /
 // 625 double slice deltas (loads issued first so their latency overlaps the rest).
-template <bool PROF>
+template <bool PROF, bool PAPER>
 __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, int n, const FeasView &F,
                                              const FamilyTables &T, double slo, long long *pacc) {
     const long long pt0 = PROF ? clock64() : 0;
@@ -327,7 +355,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
     // Warps 1.. only (3 deltas per thread): warp 0 builds the present-edge list below
     // meanwhile, so the two round trips are off its path.
     constexpr int FT = ANT - 32;
-    static_assert(3 * FT >= 650, "feasibility refresh needs 650 lookups");
+    static_assert(3 * FT >= 660, "feasibility refresh needs 650 + 10 lookups");
     bool fres[3] = {false, false, false};
     if (refresh && wid > 0) {                      // uniform across the CTA
         uint32_t obase[3], wofs[3], bit[3];
@@ -338,12 +366,16 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             int v[CLV_K];
 #pragma unroll
             for (int k = 0; k < CLV_K; ++k) v[k] = s.svec[k];
-            bool ok = t < 650;
+            bool ok = t < (PAPER ? 660 : 650);
             if (t < 25) {
                 v[t / 5] -= 1; v[t % 5] += 1;
             } else if (t < 650) {
                 const int u = t - 25;
                 v[u / 125] -= 1; v[(u / 25) % 5] -= 1; v[(u / 5) % 5] += 1; v[u % 5] += 1;
+            } else if (t < 655) {
+                v[t - 650] += 1;                   // one instance added on slice kind t - 650
+            } else if (t < 660) {
+                v[t - 655] -= 1;                   // one instance removed
             }
             ok = ok && v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[3] >= 0 && v[4] >= 0;
             // feasible(F, n, v...) split into its index arithmetic and its two loads
@@ -368,6 +400,13 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
     //     same deterministic order in every CTA of the cluster.
     const long long ptR = PROF ? clock64() : 0;
     if (wid == 0) {
+        if (PAPER && s.ub_dirty) {                 // an add / remove move changed m: new W0 bound
+            const double w0b = w0_bound(s.mcount, s.ec);
+            for (int r = lane; r < E; r += 32) s.ub[r] = s.ec.c20 / (s.svc_by_rank[r] + w0b);
+            __syncwarp();
+            if (lane == 0) s.ub_dirty = 0;
+            __syncwarp();
+        }
         int k = 0;
         for (int e0 = 0; e0 < E; e0 += 32) {
             const int e = e0 + lane;
@@ -528,6 +567,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
             const int t = threadIdx.x - 32 + q * FT;
             if (t < 25) s.feasS[t] = fres[q];
             else if (t < 650) s.feasD[t - 25] = fres[q];
+            else if (t < 660) s.feasAR[t - 650] = fres[q];
         }
         if (threadIdx.x - 32 < CLV_K) s.fsvec[threadIdx.x - 32] = s.svec[threadIdx.x - 32];
     }
@@ -583,6 +623,20 @@ template <int MODE, int EC>
 __device__ __forceinline__ void score_queued(const AnnealSmem &s, const AnnealArgs &args, const RemEnt *rp,
                                              const uint32_t *plist, uint32_t d, double mcnt, KRec &rS, KRec &rV,
                                              KRec &rP, uint64_t gchain, uint64_t k) {
+    if ((d >> 30) == 1u) {                       // paper move: add (bit 8 clear) / remove one instance
+        const int e = d & 0xFFu;
+        const bool rem = (d >> 8) & 1u;
+        const ARow &A = s.row[e];
+        const double sg = rem ? -1.0 : 1.0;      // S -/+ row: exact integers either way
+        const unsigned long long pm = rem ? (s.w[e] == 1 ? (s.pmask & ~s.rbit[e]) : s.pmask) : (s.pmask | s.rbit[e]);
+        const CandWalk cw{&s, pm, rem ? s.rk[e] : 0xFF, 0xFF, rem ? 0xFF : s.rk[e], 0xFF};
+        const int E = args.E;
+        const int ubase = E * E + (E * (E + 1) / 2) * (E * (E + 1) / 2);
+        fold<MODE, EC>(s, args, s.S[0] + sg * A.thr, s.S[1] + sg * A.acc, s.S[2] + sg * A.en, s.S[3] + sg * A.idle,
+                       s.S[4] + sg * A.t2, s.S[5] + sg * A.t3, cw, mcnt + sg, ubase + (rem ? E : 0) + e, rS, rV, rP,
+                       args.seed, gchain, k);
+        return;
+    }
     if (d >> 31) {
         const RemEnt &R = s.se[(d >> 8) & 0xFFu];
         const int a = d & 0xFFu;
@@ -634,7 +688,7 @@ __device__ __forceinline__ bool screen_keep(double f, const RemEnt &R, bool stri
 // centre did not move) and tighten with the CTA's records.  Survivors go to a per-warp queue
 // and are scored 32 at a time, so the full epilogue runs on full warps.  The records, and
 // hence every decision, are those of scoring every candidate in full.
-template <int MODE, int EC, bool PROF>
+template <int MODE, int EC, bool PROF, bool PAPER>
 __device__ __forceinline__ void score_screened(AnnealSmem &s, const AnnealArgs &args, const RemEnt *rp,
                                                const uint32_t *plist, int crank, int CL, KRec &rS, KRec &rV,
                                                KRec &rP, unsigned long long &cnt, uint64_t gchain, uint64_t k) {
@@ -703,6 +757,31 @@ __device__ __forceinline__ void score_screened(AnnealSmem &s, const AnnealArgs &
             __syncwarp();
             drain(false);
         }
+        // paper move set: one-instance add / remove (m changes: scored in full, no screen)
+        if (PAPER) {
+            const int nU = E + s.nPE;
+            for (int base = (crank * NWARP + wid) * 32; base < nU; base += CL * ANT) {
+                const int t = base + lane;
+                bool sv = false;
+                uint32_t dsc = 0;
+                if (t < nU) {
+                    if (t < E) {
+                        sv = ((mem_ok >> t) & 1ULL) && s.feasAR[s.sl[t]];
+                        dsc = 0x40000000u | (uint32_t)t;
+                    } else {
+                        const int r = s.pe_list[t - E];
+                        sv = s.feasAR[5 + s.sl[r]] != 0;
+                        dsc = 0x40000000u | 0x100u | (uint32_t)r;
+                    }
+                    cnt += sv ? 1 : 0;
+                }
+                const unsigned bal = __ballot_sync(0xFFFFFFFFu, sv);
+                if (sv) q[qn + __popc(bal & lt)] = dsc;
+                qn += __popc(bal);
+                __syncwarp();
+                drain(false);
+            }
+        }
         // score the surviving singles now: their records set the doubles' thresholds
         drain(true);
         const unsigned long long kS = warp_min_u64(rS.key), kV = warp_min_u64(rV.key);
@@ -744,7 +823,7 @@ __device__ __forceinline__ void score_screened(AnnealSmem &s, const AnnealArgs &
         };
         fetch(tb0);
         for (int base = tb0; base < tend; base += 32 * SCREEN_UNR) {
-            if (((base - tb0) & (4 * 32 * SCREEN_UNR - 1)) == 0) refresh();
+            refresh();
             uint32_t ent[SCREEN_UNR];
             int jc[SCREEN_UNR];
 #pragma unroll
@@ -793,7 +872,7 @@ __device__ __forceinline__ void score_screened(AnnealSmem &s, const AnnealArgs &
         prof_last = _now;                                                              \
     }
 
-template <int MODE, int MINB, int UNR, bool PROF = false, int EC = 0>
+template <int MODE, int MINB, int UNR, bool PROF = false, int EC = 0, bool PAPER = false>
 __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant__ AnnealArgs args) {
     long long prof_acc[PROF_SLOTS] = {};
     long long prof_last = 0;
@@ -834,6 +913,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         s.mem_ok = T.mem_ok;
         s.magicE = 0xFFFFFFFFu / (unsigned)E + 1u;
         s.magicNP = 0xFFFFFFFFu / (unsigned)(E * (E + 1) / 2) + 1u;
+        s.ubase = (unsigned)(E * E) + (unsigned)(E * (E + 1) / 2) * (unsigned)(E * (E + 1) / 2);
+        s.ub_dirty = 0;
         s.ec = args.ec[args.n_ec == 1 ? 0 : chain];
     }
     __syncthreads();
@@ -868,6 +949,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     const bool leader = (crank == 0 && tid == 0);
     double hc = 0.0;
     bool slac = false;                       // SLA class of the centre (MODE_BEST_ALL seeds)
+    double t_raw = args.t_init;              // multiplicative cooling: t_init (1 - cooling)^k
     unsigned int bk1 = 0;
     unsigned long long bk2 = 0;
     int best_step = -1, stall = 0, steps = 0, status = 0;
@@ -892,12 +974,12 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     }
     cluster.sync();                          // all CTAs started before any DSMEM traffic
     bool done = s.dec_done;
-    const double mcnt = s.mcount;
     const int G = CL * ANT;
     const int gt = crank * ANT + tid;
     const unsigned long long mem_ok = s.mem_ok;
 
     for (int k = 0; !done; ++k) {
+        const double mcnt = s.mcount;            // the centre's instance count (paper moves change it)
         PROF_MARK(0);
         bool refreshed = false;
         if (PROF) {
@@ -905,7 +987,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             for (int q = 0; q < CLV_K; ++q) refreshed |= (s.svec[q] != s.fsvec[q]);
         }
         const long long prep0 = PROF ? clock64() : 0;
-        prepare_step<PROF>(s, rp, E, n, args.F, T, s.ec.slo, prof_acc);
+        prepare_step<PROF, PAPER>(s, rp, E, n, args.F, T, s.ec.slo, prof_acc);
         if (PROF && threadIdx.x == 0 && refreshed) { prof_acc[7] += clock64() - prep0; prof_acc[8] += 1; }
         PROF_MARK(1);
         KRec rS = krec_none(), rV = krec_none(), rP = krec_none();
@@ -929,11 +1011,23 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 i += dI; a += dA;
                 if (a >= E) { a -= E; ++i; }
             }
+            if (PAPER) {                             // one-instance add / remove: hash only
+                const int nU = E + s.nPE;
+                for (int t = gt; t < nU; t += G) {
+                    const bool add = t < E;
+                    const int e = add ? t : s.pe_list[t - E];
+                    if (add ? (((mem_ok >> e) & 1ULL) && s.feasAR[s.sl[e]]) : (s.feasAR[5 + s.sl[e]] != 0)) {
+                        ++cnt;
+                        score_queued<MODE, EC>(s, args, rp, T.pair_list, 0x40000000u | (add ? 0u : 0x100u) | (uint32_t)e,
+                                               mcnt, rS, rV, rP, gchain, (uint64_t)k);
+                    }
+                }
+            }
         }
         // ---- doubles: flattened (removal entry, static list entry) space; each warp
         // owns a contiguous chunk, lanes walk it 32 apart (UNR independent items each)
         if (MODE != MODE_UNIFORM_PROPOSAL) {
-            score_screened<MODE, EC, PROF>(s, args, rp, T.pair_list, crank, CL, rS, rV, rP, cnt, gchain,
+            score_screened<MODE, EC, PROF, PAPER>(s, args, rp, T.pair_list, crank, CL, rS, rV, rP, cnt, gchain,
                                            (uint64_t)k);
         } else {
             const int lane = tid & 31, wid = tid >> 5;
@@ -1062,8 +1156,10 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 } else {
                     stall += 1;
                 }
-                const double T0 = args.t_init - (double)k * args.cooling;
+                // subtractive T_k = t_init - k cooling; multiplicative: t_raw *= (1 - cooling) each step
+                const double T0 = (args.flags & CLV_ANNEAL_MULT_COOLING) ? t_raw : args.t_init - (double)k * args.cooling;
                 const double Tk = args.t_floor >= T0 ? args.t_floor : T0;
+                t_raw = t_raw * args.cool_factor;
                 bool acc = hp <= hc;                 // Eq. 7: the draw only matters for worse moves
                 if (!acc) {
                     const double u = uniform01(derive_seed4(args.seed, gchain, (uint64_t)k, 0ULL));
@@ -1072,7 +1168,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (args.log && leader) {
                     clv_log_row row;
                     row.temp = Tk; row.f = fp; row.h = hp; row.p95_ms = Lp;
-                    row.iter = k; row.ged_from_center = (pidx < (long long)E * E) ? 2 : 4; row.sla_met = slap;
+                    const long long NPl = (long long)E * (E + 1) / 2;
+                    row.iter = k; row.sla_met = slap;
+                    row.ged_from_center = pidx < (long long)E * E ? 2 : (pidx < (long long)E * E + NPl * NPl ? 4 : 1);
                     row.accepted = acc; row.new_best = nb; row.n_neighbours = (int)total;
                     args.log[(size_t)chain * args.max_steps + k] = row;
                 }
@@ -1136,7 +1234,9 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             S4 += x * s.row[e].t2; S5 += x * s.row[e].t3;
             if (x > 0) m |= s.rbit[e];
         }
-        const Score sb = epilogue_d(S0, S1, S2, S3, S4, S5, s.mcount, s.ec, GraphWalk{&s, s.bw, s.er, m});   // moves keep m
+        int mb = 0;
+        for (int e = 0; e < E; ++e) mb += s.bw[e];  // paper moves change m: the best graph's own count
+        const Score sb = epilogue_d(S0, S1, S2, S3, S4, S5, (double)mb, s.ec, GraphWalk{&s, s.bw, s.er, m});
         r.f = sb.f; r.h = sb.h; r.p95_ms = sb.L; r.accuracy = sb.A; r.energy_wh = sb.E;
         r.sla_met = sb.sla;
         r.status = status; r.steps = steps; r.best_step = best_step;
@@ -1148,8 +1248,14 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
 template <int MODE, int MINB, int UNR, bool PROF = false>
 static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
     // branch-free divisions when every scenario keeps them exact (fast_div_safe)
-    auto kern = !a.fast_div ? anneal_kernel<MODE, MINB, UNR, PROF, 0>
-              : a.n_ec == 1 ? anneal_kernel<MODE, MINB, UNR, PROF, 2> : anneal_kernel<MODE, MINB, UNR, PROF, 1>;
+    // (the paper move set is a template flag: the SPEC-move kernels carry none of its code)
+    const bool paper = (a.flags & CLV_ANNEAL_PAPER_MOVES) != 0;
+    auto kern = paper ? (!a.fast_div ? anneal_kernel<MODE, MINB, UNR, PROF, 0, true>
+                         : a.n_ec == 1 ? anneal_kernel<MODE, MINB, UNR, PROF, 2, true>
+                                       : anneal_kernel<MODE, MINB, UNR, PROF, 1, true>)
+                      : (!a.fast_div ? anneal_kernel<MODE, MINB, UNR, PROF, 0, false>
+                         : a.n_ec == 1 ? anneal_kernel<MODE, MINB, UNR, PROF, 2, false>
+                                       : anneal_kernel<MODE, MINB, UNR, PROF, 1, false>);
     const size_t smem = sizeof(AnnealSmem) + sizeof(RemEnt) * (size_t)(a.E * (a.E + 1) / 2);
     // The attribute calls and the cluster-size search (up to 15 occupancy queries) run
     // once per (device, kernel, chains, shared bytes): a re-plan is ~1.5 ms, and these
@@ -1167,9 +1273,17 @@ static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream
         if (it != chosen.end()) { attrs_set = true; cached = it->second; }
     }
     if (!attrs_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        // The dynamic shared-memory limit is a per-function attribute: only ever raise it (a
+        // smaller family's launch must not lower it under a cached larger configuration).
+        static std::map<std::pair<int, const void *>, size_t> smem_set;
+        std::lock_guard<std::mutex> lk(mu);
+        size_t &cur = smem_set[std::make_pair(dev, reinterpret_cast<const void *>(kern))];
+        if (smem > cur) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            cur = smem;
+        }
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
     cudaLaunchConfig_t cfg = {};
@@ -1215,14 +1329,8 @@ static int env_int(const char *name, int dflt) {
 
 cudaError_t launch_anneal(const AnnealArgs &a, int cluster_size, cudaStream_t st) {
     if (a.proposal == 0) {
-        // tuning variants of the headline mode (CLV_ANNEAL_VARIANT, default 0)
+        // CLV_ANNEAL_VARIANT=9: the phase-profiling build of the headline mode
         switch (env_int("CLV_ANNEAL_VARIANT", 0)) {
-            case 1: return launch_mode<MODE_BEST_ALL, 3, 1>(a, cluster_size, st);
-            case 2: return launch_mode<MODE_BEST_ALL, 4, 1>(a, cluster_size, st);
-            case 3: return launch_mode<MODE_BEST_ALL, 3, 3>(a, cluster_size, st);
-            case 4: return launch_mode<MODE_BEST_ALL, 3, 4>(a, cluster_size, st);
-            case 5: return launch_mode<MODE_BEST_ALL, 2, 2>(a, cluster_size, st);
-            case 6: return launch_mode<MODE_BEST_ALL, 2, 4>(a, cluster_size, st);
             case 9: return launch_mode<MODE_BEST_ALL, 3, 2, true>(a, cluster_size, st);
             default: return launch_mode<MODE_BEST_ALL, 3, 2>(a, cluster_size, st);
         }

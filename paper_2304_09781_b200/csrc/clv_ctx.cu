@@ -1,5 +1,6 @@
 // clv_ctx.cu -- the C-ABI (include/clover.h): context, table staging, argument
 // validation, launch orchestration and status-code mapping.
+#include <nvtx3/nvToolsExt.h>
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -568,7 +569,8 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
     if (n_chains == 0) return CLV_OK;
     if (!ap || !(ap->t_floor > 0) || !(ap->cooling_step > 0) || ap->stall_limit < 1 || ap->max_steps < 0 ||
         ap->proposal < 0 || ap->proposal > 1 || ap->evaluate < 0 || ap->evaluate > 1 ||
-        (ap->proposal == 0 && ap->evaluate != 0))
+        (ap->proposal == 0 && ap->evaluate != 0) || (ap->flags & ~3) ||
+        ((ap->flags & CLV_ANNEAL_MULT_COOLING) && !(ap->cooling_step < 1.0)))
         return fail(ctx, CLV_ERR_CARBON_SCHED, "invalid anneal parameters");
     if (n_params != 1 && n_params != n_chains) return fail(ctx, CLV_ERR_CARBON_SCHED, "n_params must be 1 or n_chains");
     if (cluster_size < 0 || cluster_size > 16)
@@ -594,6 +596,7 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
     for (int i = 0; i < n_params; ++i)
         if (!fast_div_safe(ecs[i], ctx->fam[family].lat95, ctx->fam[family].svc, ctx->fam[family].E)) a.fast_div = 0;
     a.t_init = ap->t_init; a.cooling = ap->cooling_step; a.t_floor = ap->t_floor;
+    a.cool_factor = 1.0 - ap->cooling_step; a.flags = ap->flags;
     a.stall_limit = ap->stall_limit; a.max_steps = ap->max_steps; a.proposal = ap->proposal; a.evaluate = ap->evaluate;
     a.n = n; a.n_chains = n_chains; a.E = ctx->fam[family].E; a.chain_base = chain_base; a.seed = seed;
     a.start_w = start_w_dev; a.res = results_dev; a.best_w = best_w_dev; a.final_w = final_w_dev; a.log = log_dev;
@@ -639,6 +642,11 @@ int clv_replan(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
                int cluster_size, clv_chain_result *results_host, uint16_t *best_w_host, uint16_t *final_w_host,
                clv_record *record_host, void *stream) {
     if (!ctx) return CLV_ERR_CARBON_SCHED;
+    // one NVTX range per re-plan (visible in nsys / ncu --nvtx timelines); header-only NVTX3
+    struct NvtxRange {
+        NvtxRange() { nvtxRangePushA("clv_replan"); }
+        ~NvtxRange() { nvtxRangePop(); }
+    } nvtx_range;
     int rc = need_family(ctx, family);
     if (rc) return rc;
     if (n_chains < 1) return fail(ctx, CLV_ERR_CARBON_SCHED, "a re-plan needs at least one chain");

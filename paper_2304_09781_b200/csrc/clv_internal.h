@@ -133,7 +133,9 @@ struct AnnealArgs {
     EvalConst ec0;                  // = ec[0] when n_ec == 1 (kernel-parameter copy)
     int fast_div;                   // every scenario and the family's lat95 satisfy fast_div_safe()
     double t_init, cooling, t_floor;
+    double cool_factor;             // 1 - cooling (multiplicative cooling)
     int stall_limit, max_steps, proposal, evaluate;
+    int flags;                      // CLV_ANNEAL_MULT_COOLING | CLV_ANNEAL_PAPER_MOVES
     int n, n_chains, E;
     long long chain_base;
     uint64_t seed;

@@ -84,6 +84,10 @@ class CloverEngine:
 
     Profiles are registered as families (up to 8); feasibility tables cover
     fleets of up to ``n_max`` GPUs (clv_build_feasibility, K6).
+
+    The context's scratch (selection partials, move log, re-plan staging) is shared by
+    all calls, so one engine must be driven from one CUDA stream at a time; use one
+    engine per concurrent stream (include/clover.h).
     """
 
     def __init__(self, topology: MigTopology = DEFAULT_TOPOLOGY, device: Optional[int] = None,
@@ -384,7 +388,8 @@ class CloverEngine:
             raise CarbonSchedError("start graphs need %d edge weights" % E)
         params = (N.EvalParams * len(scenarios))(*[eval_params(s) for s in scenarios])
         apc = N.AnnealParamsC(ap.t_init, ap.cooling_step, ap.t_floor, ap.stall_limit, ap.step_limit(),
-                              1 if ap.proposal == "uniform" else 0, 1 if ap.evaluate == "proposal" else 0)
+                              1 if ap.proposal == "uniform" else 0, 1 if ap.evaluate == "proposal" else 0,
+                              ap.flags())
         steps = ap.step_limit()
         if out is None or out.n_chains != n_chains or (log and out.log is None):
             out = AnnealBatch(torch.empty(n_chains * CHAIN_DTYPE.itemsize, dtype=torch.uint8, device=dev),
@@ -420,7 +425,8 @@ class CloverEngine:
         else:
             params = (N.EvalParams * len(scenarios))(*[eval_params(x) for x in scenarios])
             apc = N.AnnealParamsC(ap.t_init, ap.cooling_step, ap.t_floor, ap.stall_limit, ap.step_limit(),
-                                  1 if ap.proposal == "uniform" else 0, 1 if ap.evaluate == "proposal" else 0)
+                                  1 if ap.proposal == "uniform" else 0, 1 if ap.evaluate == "proposal" else 0,
+                              ap.flags())
             self._replan_args = (scenarios[0], ap, params, apc) if len(scenarios) == 1 else None
         n = scenarios[0].n_gpus
         self.ensure_feasibility(n)

@@ -160,7 +160,15 @@ class AnnealParams:
     configs[1]); "proposal" scores only the proposal (SPEC-literal anneal).
     ``max_steps`` bounds steps; the SPEC's time budget additionally bounds the
     evaluation count in "proposal" mode (eval_cost_s per evaluation).
+    ``move_set``: "spec" -- the m-invariant GED <= 4 swap / slice moves (SPEC:196-204);
+    "paper" -- also one-instance add / remove (GED 1).  ``cooling``:
+    "subtractive" (T_k = max(t_floor, t_init - k cooling_step)) or "multiplicative"
+    (T_k = max(t_floor, t_init (1 - cooling_step)^k), both SPEC:492).
     """
+
+    def flags(self) -> int:
+        """clv_anneal_params.flags (include/clover.h)."""
+        return (1 if self.cooling == "multiplicative" else 0) | (2 if self.move_set == "paper" else 0)
 
     t_init: float = 1.0
     cooling_step: float = 0.05
@@ -171,8 +179,12 @@ class AnnealParams:
     max_steps: int = 64
     proposal: str = "best"
     evaluate: str = "all"
+    move_set: str = "spec"          # "paper": + unit instance add / remove
+    cooling: str = "subtractive"    # "multiplicative": T_k = t_init (1 - cooling_step)^k
 
     def __post_init__(self) -> None:
+        if self.move_set not in ("spec", "paper") or self.cooling not in ("subtractive", "multiplicative"):
+            raise CarbonSchedError("unknown move set / cooling mode")
         if not self.t_floor > 0 or not self.cooling_step > 0 or self.t_init < self.t_floor:
             raise CarbonSchedError("invalid temperature schedule")
         if self.stall_limit < 1 or self.max_steps < 0:

@@ -303,7 +303,16 @@ def blover_search(n: int, profile: ProfileTable, workload: Workload, ci: float, 
     eng = engine or default_engine(profile.topology)
     ap = ap or AnnealParams(proposal="uniform", evaluate="proposal")
     sc = scenario_for(n, workload, ci, obj)
-    seed = _seed_of(rng)
+    fc, best, log = blover_run(eng, profile, sc, n, ap, _seed_of(rng))
+    return EvalResult(build_graph(fc, profile), best["accuracy"], best["energy_wh"], best["p95_ms"],
+                      best["f"], best["h"], bool(best["sla_met"])), log
+
+
+def blover_run(eng: CloverEngine, profile: ProfileTable, sc: Scenario, n: int, ap: AnnealParams, seed: int):
+    """BLOVER's draws under anneal's termination rules: at most max_steps + 1
+    draws (bounded by the time budget at eval_cost_s each), stop after stall_limit draws
+    without a new best.  Returns (winner FleetConfig, its full score, per-draw log); the log's
+    length is the evaluation count."""
     budget = ap.max_steps + 1
     if ap.eval_cost_s > 0 and math.isfinite(ap.time_budget_s):
         budget = min(budget, max(1, math.ceil(ap.time_budget_s / ap.eval_cost_s)))
@@ -324,8 +333,7 @@ def blover_search(n: int, profile: ProfileTable, workload: Workload, ci: float, 
             break
     fc = eng.sweep_decode(pods, seed, bi)[0]
     best, _ = eng.score_fleets([fc], profile, sc)
-    return EvalResult(build_graph(fc, profile), best["accuracy"], best["energy_wh"], best["p95_ms"],
-                      best["f"], best["h"], bool(best["sla_met"])), log
+    return fc, best, log
 
 
 def random_fleets(engine: CloverEngine, profile: ProfileTable, n: int, seed: int, count: int,

@@ -34,7 +34,7 @@ class Best(ctypes.Structure):
 class AnnealParams(ctypes.Structure):
     _fields_ = [("t_init", ctypes.c_double), ("cooling_step", ctypes.c_double), ("t_floor", ctypes.c_double),
                 ("stall_limit", ctypes.c_int32), ("max_steps", ctypes.c_int32), ("proposal", ctypes.c_int32),
-                ("evaluate", ctypes.c_int32)]
+                ("evaluate", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
 
 class ChainResult(ctypes.Structure):
@@ -123,7 +123,7 @@ def test_reference_style_ctypes_binding_replans(engine):
                        sc.rho_sat, 1 if sc.strict_eq6 else 0, 64, float("inf"))
         ap_py = bench.anneal_params(20)
         ap = AnnealParams(ap_py.t_init, ap_py.cooling_step, ap_py.t_floor, ap_py.stall_limit, ap_py.step_limit(),
-                          0, 0)
+                          0, 0, 0)
         starts = bench.make_starts(prof, 3, 0, 24, 0.75)
         m, E = starts.shape
         w = (ctypes.c_uint16 * (m * E))(*[int(x) for x in starts.reshape(-1)])

@@ -86,3 +86,37 @@ def test_neighbour_spec_examples():
     nb = enumerate_neighbours(w, np.ones(10, bool), 2, 1, feas)
     target = w.copy(); target[4] = 6; target[9] = 1
     assert any(np.array_equal(g, target) for g in nb.W)
+
+
+def test_paper_move_set_adds_unit_moves():
+    """moves="paper" = the SPEC neighbourhood plus every realizable, memory-feasible graph at
+    L1 distance 1 (one instance added or removed), with the documented indices."""
+    import numpy as np
+    from oracle.feasibility import FeasOracle
+    from oracle.neighbours import enumerate_neighbours
+    from oracle.tables import OracleTables
+    from paper_2304_09781_b200.mig import DEFAULT_TOPOLOGY
+    from paper_2304_09781_b200.profiles import synthetic_profile
+    from tests.helpers import random_fleet_graphs
+    prof = synthetic_profile("bert")
+    T = OracleTables.from_profile(prof)
+    n = 3
+    feas = FeasOracle(DEFAULT_TOPOLOGY, n)
+    E = T.E
+    NP = E * (E + 1) // 2
+    for w in random_fleet_graphs(T, n, 6, seed=9):
+        spec = enumerate_neighbours(w, T.mem_ok, T.V, n, feas)
+        paper = enumerate_neighbours(w, T.mem_ok, T.V, n, feas, moves="paper")
+        extra = paper.idx >= E * E + NP * NP
+        assert np.array_equal(paper.idx[~extra], spec.idx)
+        unit = set()
+        for e in range(E):
+            for d in (1, -1):
+                g = w.copy(); g[e] += d
+                if g[e] < 0 or (d > 0 and not T.mem_ok[e]):
+                    continue
+                svec = g.reshape(T.V, 5).sum(axis=0)
+                if feas.feasible(svec, n):
+                    unit.add(tuple(g))
+        assert {tuple(x) for x in paper.W[extra]} == unit
+        assert (np.abs(paper.W[extra] - w).sum(axis=1) == 1).all() and (paper.ged[extra] == 1).all()

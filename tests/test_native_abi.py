@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), name
         assert name in N.SIGNATURES, name
-    assert lib.clv_abi_version() == 2
+    assert lib.clv_abi_version() == 3
 
 
 def test_host_derive_seed_through_abi():
