@@ -153,7 +153,8 @@ struct __align__(16) AnnealSmem {
     KRec slS[2][MAXCL], slV[2][MAXCL], slP[2][MAXCL];   // [step parity][cluster rank]
     unsigned long long slc[2][MAXCL];
     int dec_done;
-    unsigned long long prof_surv;          // debug profile: screened-in double moves
+    unsigned long long prof_surv;          // debug profile: candidates scored in full
+    unsigned long long prof_surv1;         // debug profile: of which singles and unit moves
     int bw[CLV_MAX_EDGES];                 // best graph (rank 0)
 };
 
@@ -783,6 +784,7 @@ __device__ __forceinline__ void score_screened(AnnealSmem &s, const AnnealArgs &
             }
         }
         // score the surviving singles now: their records set the doubles' thresholds
+        if (PROF && lane == 0) atomicAdd(&s.prof_surv1, (unsigned long long)(nsurv + qn));
         drain(true);
         const unsigned long long kS = warp_min_u64(rS.key), kV = warp_min_u64(rV.key);
         thS = kS < thS ? kS : thS;
@@ -936,7 +938,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         int cnt = 0;
         for (int e = 0; e < E; ++e) { cnt += s.w[e]; s.wr[s.rk[e]] = (double)s.w[e]; }
         s.mcount = (double)cnt;
-        s.seedS = ~0ULL; s.seedO = ~0ULL; s.prof_surv = 0ULL;
+        s.seedS = ~0ULL; s.seedO = ~0ULL; s.prof_surv = 0ULL; s.prof_surv1 = 0ULL;
         s.thS_sh = ~0ULL; s.thO_sh = ~0ULL;
     }
     __syncthreads();
@@ -1110,6 +1112,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
                 if (krec_less(s.slP[par][q].key, s.slP[par][q].idx, Pr)) Pr = s.slP[par][q];
                 total += s.slc[par][q];
             }
+            const long long pm0 = PROF ? clock64() : 0;
+            if (PROF) prof_acc[17] += pm0 - prof_last;
             long long mv = NOIDX;
             int fin = 0;
             if (total == 0) {
@@ -1194,6 +1198,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             }
             if (!fin && k + 1 >= args.max_steps) { status = 0; fin = 1; }
             const long long ap0 = PROF ? clock64() : 0;
+            if (PROF) prof_acc[18] += ap0 - pm0;
             if (mv != NOIDX) apply_move(s, E, mv);
             s.dec_done = fin;
             if (PROF) prof_acc[9] += clock64() - ap0;
@@ -1206,7 +1211,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     }
     // Keep every CTA's shared memory alive until no peer can touch it over DSMEM.
     cluster.sync();
-    if (PROF && threadIdx.x == 0) prof_acc[16] = (long long)s.prof_surv;
+    if (PROF && threadIdx.x == 0) { prof_acc[16] = (long long)s.prof_surv; prof_acc[19] = (long long)s.prof_surv1; }
     if (PROF && threadIdx.x == 0 && args.prof)
         for (int q = 0; q < PROF_SLOTS; ++q) args.prof[((size_t)blockIdx.x) * PROF_SLOTS + q] = prof_acc[q];
 

@@ -54,3 +54,5 @@ print("feasibility refresh in %.1f%% of steps; prepare cycles per refresh step %
 surv = buf[:, :, 16].sum()
 ev = b.host()["results"]["evals"].astype(np.float64).sum()
 print("screen: %d double moves scored in full of %d candidates (%.2f%%)" % (surv, ev, 100.0 * surv / ev))
+print("  of which singles / unit moves (warm-up): %d" % buf[:, :, 19].sum())
+print("leader: record merge %d, decision until apply %d cycles per step" % (per_step(buf[:, 0, 17]), per_step(buf[:, 0, 18])))
