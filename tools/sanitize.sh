@@ -8,10 +8,11 @@ from paper_2304_09781_b200.objective import AnnealParams
 import bench
 eng=CloverEngine(n_max=64); prof=synthetic_profile("efficientnet")
 sc=eng.calibrate(prof,64,350.0,0.5)
-st=bench.make_starts(eng,prof,1,0,3)
+st=bench.make_starts(prof,1,0,3,0.75)
 for mode in ("best","uniform"):
     b=eng.anneal(st,prof,sc,AnnealParams(max_steps=3, proposal=mode),1,cluster=2)
 b=eng.anneal(st,prof,sc,AnnealParams(max_steps=3, proposal="uniform", evaluate="proposal"),1,cluster=3)
+b=eng.anneal(st,prof,sc,AnnealParams(max_steps=3, move_set="paper", cooling="multiplicative"),1,cluster=3)
 best,_=eng.score_graphs(st,prof,sc)
 eng.replan(st,prof,sc,AnnealParams(max_steps=3),1,cluster=0)
 pr2=synthetic_profile("resnet"); s2=eng.calibrate(pr2,16,300.0,0.5)
@@ -28,7 +29,9 @@ for f in (fl[:5],):
     try: eng.score_x(xp,np.concatenate(xvs),off,64,prof,sc)
     except Exception as e: print("expected:", type(e).__name__, e)
 torch.cuda.synchronize(); print("ok")'
+mkdir -p gpurun_out
 for tool in memcheck racecheck synccheck; do
   echo "== $tool"
-  timeout 900 compute-sanitizer --tool $tool --print-limit 10 python -c "$PY" 2>&1 | tail -4
+  timeout 900 compute-sanitizer --tool $tool --print-limit 10 python -c "$PY" > gpurun_out/sanitize_$tool.txt 2>&1
+  tail -4 gpurun_out/sanitize_$tool.txt
 done
