@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--workload", default="c2", choices=["c0", "c1", "c2", "c3", "c4", "des"],
                     help="c2 (default) is the headline; c0/c1/c4 are the other BASELINE configs")
     ap.add_argument("--sweep", type=int, default=1_000_000_000, help="c4: candidates per sweep (whole job)")
+    ap.add_argument("--c1-starts", type=int, default=12,
+                    help="c1: chains per lambda (BASE + perturbations of BASE); 1 = one chain per lambda")
     return ap.parse_args()
 
 
@@ -569,9 +571,9 @@ def _c0_eval(rng):
 
 def _c1_chain(a):
     from oracle.anneal import anneal_chain
-    w0, lam_i, seed, max_steps = a
+    w0, chain, lam_i, seed = a
     t0 = time.perf_counter()
-    out = anneal_chain(w0, 8, _C0["T"], _C0["scs"][lam_i], _C0["ap"], seed, lam_i, _C0["feas"])
+    out = anneal_chain(w0, 8, _C0["T"], _C0["scs"][lam_i], _C0["ap"], seed, chain, _C0["feas"])
     return out, time.perf_counter() - t0
 
 
@@ -735,29 +737,40 @@ def run_other(args, rank, world, local):
         from paper_2304_09781_b200.objective import AnnealParams
         ap = AnnealParams(max_steps=args.max_steps)
         V = prof.variant_count
-        start = np.zeros((len(lams), V * 5), dtype=np.uint16)
-        start[:, (V - 1) * 5] = n
+        # chain c: lambda c % 11, start c // 11 (0 = BASE, then perturbations of BASE): a multi-start
+        # lambda sweep that fills the GPU (one chain per lambda leaves a B200 idle)
+        from paper_2304_09781_b200.search import base_config, perturbed_fleets
+        from paper_2304_09781_b200.graph import build_graph
+        K = max(1, args.c1_starts)
+        base = np.zeros(V * 5, dtype=np.uint16)
+        base[(V - 1) * 5] = n
+        pert = [np.array(build_graph(f, prof).weights, dtype=np.uint16)
+                 for f in perturbed_fleets(base_config(n, prof), prof, SEED, K - 1, 0, 0.5)] if K > 1 else []
+        starts_k = [base] + pert
+        start = np.array([starts_k[c // len(lams)] for c in range(K * len(lams))], dtype=np.uint16)
+        scs_c = [scs[c % len(lams)] for c in range(len(start))]
         sd = torch.from_numpy(start.view(np.int16)).cuda().view(torch.uint16)
         def step(s):
-            b = eng.anneal(sd, prof, scs, ap, SEED + s, chain_base=rank * len(lams))
+            b = eng.anneal(sd, prof, scs_c, ap, SEED + s, chain_base=rank * len(start))
             exchange_record(eng, eng.select_chains(b))
             return b
         res = _timed_steps(step, args.steps, args.warmup, flush)
         per_step = [int(r[1].host()["results"]["evals"].sum()) for r in res]
-        cfg = "c1: n=8 GPUs, EfficientNet B1-B7 (V=7), lambda sweep 0..1 (11 chains from BASE, one per lambda), " \
-              "full GED<=4 neighbourhood per step, to termination; replicas across GPUs"
+        cfg = "c1: n=8 GPUs, EfficientNet B1-B7 (V=7), lambda sweep 0..1: %d chains = 11 lambdas x %d starts (BASE " \
+              "and perturbations of BASE), full GED<=4 neighbourhood per step, to termination; replicas across " \
+              "GPUs" % (len(start), K)
         scaling = "weak"
         et, ee = [], 0
         for s in range(args.warmup + args.steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            r = anneal_chains(eng, start, prof, scs, ap, SEED + s, chain_base=rank * len(lams))
+            r = anneal_chains(eng, start, prof, scs_c, ap, SEED + s, chain_base=rank * len(start))
             et.append(time.perf_counter() - t0)
             if s >= args.warmup:
                 ee += r.evals
         E = V * 5
-        e2e = {"value": ee / sum(et[args.warmup:]), "unit": UNIT, "h2d_bytes_per_step": len(lams) * E * 2,
-               "d2h_bytes_per_step": len(lams) * 80 + 2 * len(lams) * E * 2 + 32,
+        e2e = {"value": ee / sum(et[args.warmup:]), "unit": UNIT, "h2d_bytes_per_step": len(start) * E * 2,
+               "d2h_bytes_per_step": len(start) * 80 + 2 * len(start) * E * 2 + 32,
                "path": "search.anneal_chains -> clv_replan (host starts in, host results out)"}
         if cpu_on:
             from oracle.tables import OracleTables
@@ -766,19 +779,19 @@ def run_other(args, rank, world, local):
             T = OracleTables.from_profile(prof)
             _C0.update(T=T, scs=[calibrate(prof, T, n, 400.0, l) for l in lams], ap=ap,
                        feas=FeasOracle(DEFAULT_TOPOLOGY, n))
-            jobs = [(start[i].astype(np.int64), i, SEED + args.warmup, args.max_steps) for i in range(len(lams))]
+            jobs = [(start[c].astype(np.int64), c, c % len(lams), SEED + args.warmup) for c in range(len(start))]
             t0 = time.perf_counter()
             outs1 = [_c1_chain(j) for j in jobs]
             t1 = time.perf_counter() - t0
             ev1 = sum(o.evals for o, _ in outs1)
             cpu = {"value": ev1 / t1, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
-                   "sample": "the 11 lambda chains of the first timed step by oracle/anneal.py, %d candidates in "
-                             "%.2f s" % (ev1, t1), "replan_tts_s": t1}
+                   "sample": "all %d chains of the first timed step by oracle/anneal.py, %d candidates in "
+                             "%.2f s" % (len(jobs), ev1, t1), "replan_tts_s": t1}
             t0 = time.perf_counter()
             outsN = _pool_map(_c1_chain, jobs, min(cores, len(jobs)))
             t2 = time.perf_counter() - t0
             cpu_all = {"value": ev1 / t2, "unit": UNIT, "cores": min(cores, len(jobs)), "kind": "port",
-                       "cpu_model": cpu_model(), "sample": "same 11 chains, one process per chain",
+                       "cpu_model": cpu_model(), "sample": "same %d chains in a process pool" % len(jobs),
                        "replan_tts_s": t2}
             parity = chain_parity([o for o, _ in outs1], res[0][1])
             wsample = _chain_walk_stats([o for o, _ in outs1], T, _C0["scs"][5], n)

@@ -9,8 +9,9 @@ for w in ${WORKLOADS:-c0 c1 c4 c3}; do
   timeout 1200 python bench.py --workload $w $A > gpurun_out/${TAG}_$w.json 2> gpurun_out/${TAG}_$w.err
 done
 if [ -n "$WITH_C2" ]; then
-  timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/${TAG}_c2.json 2> gpurun_out/${TAG}_c2.err
+  timeout 900 python bench.py > gpurun_out/${TAG}_c2.json 2> gpurun_out/${TAG}_c2.err
   timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err
+  timeout 600 python tools/bench_kernels.py > gpurun_out/${TAG}_kernels.json 2> gpurun_out/${TAG}_kernels.err
 fi
 for f in gpurun_out/${TAG}_*.json; do echo "== $f"; tail -c 1500 $f; echo; done
 for f in gpurun_out/${TAG}_*.err; do echo "== $f"; tail -5 $f; done
