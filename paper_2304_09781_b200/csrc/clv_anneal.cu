@@ -361,23 +361,30 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
     if (refresh && wid > 0) {                      // uniform across the CTA
         uint32_t obase[3], wofs[3], bit[3];
         bool cand[3];
+        int sv[CLV_K];
+#pragma unroll
+        for (int k = 0; k < CLV_K; ++k) sv[k] = s.svec[k];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             const int t = threadIdx.x - 32 + q * FT;
-            int v[CLV_K];
-#pragma unroll
-            for (int k = 0; k < CLV_K; ++k) v[k] = s.svec[k];
+            // removed / added slice kinds of delta t (-1 = none); the delta vector is formed with
+            // constant indices only (a dynamically indexed array would live in local memory)
+            int r1 = -1, r2 = -1, a1 = -1, a2 = -1;
             bool ok = t < (PAPER ? 660 : 650);
             if (t < 25) {
-                v[t / 5] -= 1; v[t % 5] += 1;
+                r1 = t / 5; a1 = t % 5;
             } else if (t < 650) {
                 const int u = t - 25;
-                v[u / 125] -= 1; v[(u / 25) % 5] -= 1; v[(u / 5) % 5] += 1; v[u % 5] += 1;
+                r1 = u / 125; r2 = (u / 25) % 5; a1 = (u / 5) % 5; a2 = u % 5;
             } else if (t < 655) {
-                v[t - 650] += 1;                   // one instance added on slice kind t - 650
+                a1 = t - 650;                      // one instance added on slice kind t - 650
             } else if (t < 660) {
-                v[t - 655] -= 1;                   // one instance removed
+                r1 = t - 655;                      // one instance removed
             }
+            int v[CLV_K];
+#pragma unroll
+            for (int k = 0; k < CLV_K; ++k)
+                v[k] = sv[k] - (k == r1) - (k == r2) + (k == a1) + (k == a2);
             ok = ok && v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[3] >= 0 && v[4] >= 0;
             // feasible(F, n, v...) split into its index arithmetic and its two loads
             ok = ok && v[0] <= n && (v[0] == 0 || F.has7g);
