@@ -334,6 +334,49 @@ __device__ __forceinline__ void pen_factors(double lb, double slo, float &pu, fl
     pl = cv ? __double2float_rd(((double)lf / slo) * (1.0 - 0x1p-40)) : 0.0f;
 }
 
+// apply_move by a whole warp: lanes 0-5 update one centre sum each, lane 6 the weights, the
+// slice vector and the presence mask (SPEC moves); unit moves take the serial path on lane 0.
+__device__ inline void apply_move_warp(AnnealSmem &s, int E, long long idx, int lane) {
+    int r1, r2, a1, a2;
+    decode_move(s, E, idx, r1, r2, a1, a2);
+    if (r1 == 0xFF || a1 == 0xFF) {
+        if (lane == 0) apply_move(s, E, idx);
+        __syncwarp();
+        return;
+    }
+    if (lane < 6) {
+        const double R1 = reinterpret_cast<const double *>(&s.row[r1])[lane];
+        const double A1 = reinterpret_cast<const double *>(&s.row[a1])[lane];
+        const double R2 = r2 != 0xFF ? reinterpret_cast<const double *>(&s.row[r2])[lane] : 0.0;
+        const double A2 = a2 != 0xFF ? reinterpret_cast<const double *>(&s.row[a2])[lane] : 0.0;
+        s.S[lane] = s.S[lane] + ((A1 + A2) - (R1 + R2));   // same op order as apply_move
+    } else if (lane == 6) {
+        const bool two = r2 != 0xFF;
+        const int wr1 = s.w[r1], wa1 = s.w[a1];
+        const int wr2 = two ? s.w[r2] : 0, wa2 = two ? s.w[a2] : 0;
+        unsigned long long m = s.pmask;
+        const unsigned long long br1 = s.rbit[r1], ba1 = s.rbit[a1];
+        const unsigned long long br2 = two ? s.rbit[r2] : 0ULL, ba2 = two ? s.rbit[a2] : 0ULL;
+        const int nr1 = wr1 - 1 - ((two && r2 == r1) ? 1 : 0);
+        const int nr2 = two ? ((r2 == r1) ? nr1 : wr2 - 1) : 1;
+        const int na1 = wa1 + 1 + ((two && a2 == a1) ? 1 : 0);
+        s.w[r1] = nr1;
+        s.w[a1] = na1;
+        if (two) { s.w[r2] = nr2; s.w[a2] = (a2 == a1) ? na1 : wa2 + 1; }
+        s.wr[s.rk[r1]] = (double)s.w[r1];
+        s.wr[s.rk[a1]] = (double)s.w[a1];
+        if (two) { s.wr[s.rk[r2]] = (double)s.w[r2]; s.wr[s.rk[a2]] = (double)s.w[a2]; }
+        const int kr1 = r1 % CLV_K, ka1 = a1 % CLV_K, kr2 = two ? r2 % CLV_K : -1, ka2 = two ? a2 % CLV_K : -1;
+#pragma unroll
+        for (int k = 0; k < CLV_K; ++k)
+            s.svec[k] += (k == ka1) + (k == ka2) - (k == kr1) - (k == kr2);
+        if (nr1 == 0) m &= ~br1;
+        if (nr2 == 0) m &= ~br2;
+        s.pmask = m | ba1 | ba2;
+    }
+    __syncwarp();
+}
+
 // Per-step tables: deterministic ordered compaction of the removal pairs (every
 // CTA of the cluster must build identical tables because the cluster partitions
 // the move space by table position), the present-edge entries, and -- only when
@@ -1108,17 +1151,20 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         PROF_MARK(3);
         cluster.sync();
         PROF_MARK(4);
-        // ---- every CTA (thread 0): best tracking, Eq. 7, termination; rank 0 keeps outputs
-        if (tid == 0) {
+        // ---- warp 0 merges the cluster's records (lane q: CTA q), then thread 0: best tracking,
+        // Eq. 7, termination (every CTA redundantly; rank 0 keeps outputs); warp 0 applies the move
+        KRec Sr = krec_none(), Vr = krec_none(), Pr = krec_none();
+        unsigned long long total = 0;
+        if (tid < 32) {
             const int par = k & 1;
-            KRec Sr = krec_none(), Vr = krec_none(), Pr = krec_none();
-            unsigned long long total = 0;
-            for (int q = 0; q < CL; ++q) {
-                if (krec_less(s.slS[par][q].key, s.slS[par][q].idx, Sr)) Sr = s.slS[par][q];
-                if (krec_less(s.slV[par][q].key, s.slV[par][q].idx, Vr)) Vr = s.slV[par][q];
-                if (krec_less(s.slP[par][q].key, s.slP[par][q].idx, Pr)) Pr = s.slP[par][q];
-                total += s.slc[par][q];
-            }
+            const KRec a = tid < CL ? s.slS[par][tid] : krec_none();
+            const KRec b = tid < CL ? s.slV[par][tid] : krec_none();
+            if (MODE != MODE_UNIFORM_PROPOSAL) { Sr = krec_min_redux(a); Vr = krec_min_redux(b); }
+            if (MODE != MODE_BEST_ALL) Pr = krec_min_warp<true>(tid < CL ? s.slP[par][tid] : krec_none());
+            total = __reduce_add_sync(0xFFFFFFFFu, tid < CL ? (unsigned)s.slc[par][tid] : 0u);
+        }
+        long long mv_w = NOIDX;
+        if (tid == 0) {
             const long long pm0 = PROF ? clock64() : 0;
             if (PROF) prof_acc[17] += pm0 - prof_last;
             long long mv = NOIDX;
@@ -1206,9 +1252,13 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
             if (!fin && k + 1 >= args.max_steps) { status = 0; fin = 1; }
             const long long ap0 = PROF ? clock64() : 0;
             if (PROF) prof_acc[18] += ap0 - pm0;
-            if (mv != NOIDX) apply_move(s, E, mv);
+            mv_w = mv;
             s.dec_done = fin;
             if (PROF) prof_acc[9] += clock64() - ap0;
+        }
+        if (tid < 32) {
+            const long long mvb = __shfl_sync(0xFFFFFFFFu, mv_w, 0);
+            if (mvb != NOIDX) apply_move_warp(s, E, mvb, tid);
         }
         PROF_MARK(5);
         __syncthreads();
