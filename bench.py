@@ -147,14 +147,36 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def fp64_peak_tflops():
-    """Measured FP64 FMA peak of this B200 (tools/microbench.cu), TFLOP/s."""
+_PEAK = {}
+
+
+def fp64_peak_tflops(device=0):
+    """Measured FP64 FMA peak of this B200 (tools/microbench.cu): the burst figure (best of 5
+    launches) as the roofline denominator, plus a ~1 s sustained run with nvidia-smi clocks
+    sampled during it, so the denominator carries its own clock record."""
+    if "v" in _PEAK:
+        return _PEAK["v"], _PEAK["src"]
     try:
         import ctypes
         lib = ctypes.CDLL(os.path.join(ROOT, "tools", "libclv_microbench.so"))
         lib.clv_mb_fp64_tflops.restype = ctypes.c_double
         lib.clv_mb_fp64_tflops.argtypes = [ctypes.c_int]
-        return float(lib.clv_mb_fp64_tflops(0)), "measured (tools/microbench.cu DFMA loop)"
+        burst = float(lib.clv_mb_fp64_tflops(device))
+        src = "measured (tools/microbench.cu DFMA loop, burst best of 5)"
+        try:
+            lib.clv_mb_fp64_tflops_sustained.restype = ctypes.c_double
+            lib.clv_mb_fp64_tflops_sustained.argtypes = [ctypes.c_int, ctypes.c_double]
+            sampler = ClockSampler(device, "/tmp/clv_fp64_peak_clocks.csv")
+            sampler.wait_first()
+            t0 = time.time()
+            sus = float(lib.clv_mb_fp64_tflops_sustained(device, 1.0))
+            clk = sampler.stop(t0, time.time())
+            src += "; sustained 1 s: %.2f TFLOP/s at SM %s MHz (max %s), reasons %s" % (
+                sus, clk.get("sm_mhz"), clk.get("sm_max_mhz"), clk.get("reasons"))
+        except Exception as exc:  # pragma: no cover
+            src += "; sustained run unavailable: %s" % exc
+        _PEAK.update(v=burst, src=src)
+        return burst, src
     except Exception as exc:  # pragma: no cover
         return None, "unavailable: %s" % exc
 

@@ -39,3 +39,35 @@ extern "C" double clv_mb_fp64_tflops(int device) {
     double flops = 2.0 * 8.0 * (double)iters * threads * blocks;
     return flops / (best * 1e-3) / 1e12;
 }
+
+// Back-to-back DFMA launches for about `seconds` (so a clock sampler sees the load): returns the
+// median rate over the launches.
+extern "C" double clv_mb_fp64_tflops_sustained(int device, double seconds) {
+    cudaSetDevice(device);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    double *out;
+    cudaMalloc(&out, 8);
+    const int threads = 256, blocks = sms * 8, iters = 1 << 14;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    dfma_loop<<<blocks, threads>>>(out, 256, 0.999999, 1e-7);
+    float ms_all[4096];
+    int n = 0;
+    double spent = 0.0;
+    while (spent < seconds * 1e3 && n < 4096) {
+        cudaEventRecord(e0);
+        dfma_loop<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms_all[n], e0, e1);
+        spent += ms_all[n];
+        ++n;
+    }
+    cudaFree(out);
+    // median
+    for (int i = 1; i < n; ++i) { float v = ms_all[i]; int j = i - 1; while (j >= 0 && ms_all[j] > v) { ms_all[j + 1] = ms_all[j]; --j; } ms_all[j + 1] = v; }
+    const double med = ms_all[n / 2];
+    const double flops = 2.0 * 8.0 * (double)iters * threads * blocks;
+    return flops / (med * 1e-3) / 1e12;
+}
