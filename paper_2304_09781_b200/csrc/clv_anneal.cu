@@ -1394,7 +1394,7 @@ cudaError_t launch_anneal(const AnnealArgs &a, int cluster_size, cudaStream_t st
         // CLV_ANNEAL_VARIANT=9: the phase-profiling build of the headline mode
         switch (env_int("CLV_ANNEAL_VARIANT", 0)) {
             case 9: return launch_mode<MODE_BEST_ALL, 3, 2, true>(a, cluster_size, st);
-            default: return launch_mode<MODE_BEST_ALL, 3, 2>(a, cluster_size, st);
+            default: return launch_mode<MODE_BEST_ALL, 2, 2>(a, cluster_size, st);
         }
     }
     if (a.evaluate == 0) return launch_mode<MODE_UNIFORM_ALL, 3, 1>(a, cluster_size, st);
