@@ -33,7 +33,7 @@ namespace cg = cooperative_groups;
 
 namespace clv {
 
-constexpr int ANT = 256;                  // threads per CTA
+constexpr int ANT = 320;                  // threads per CTA
 constexpr int NWARP = ANT / 32;
 constexpr int MAXP = CLV_MAX_EDGES * (CLV_MAX_EDGES + 1) / 2;   // 820 removal pairs
 constexpr int MAXCL = 16;
@@ -389,7 +389,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int NP = E * (E + 1) / 2;
     constexpr int PER = (MAXP + ANT - 1) / ANT;    // consecutive pairs per thread (4 at E <= 40)
-    static_assert(PER == 4, "pair split assumes <= 1024 removal pairs");
+    static_assert(PER <= 4, "pair split assumes <= 4 removal pairs per thread");
     bool refresh = false;
 #pragma unroll
     for (int k = 0; k < CLV_K; ++k) refresh |= (s.svec[k] != s.fsvec[k]);
@@ -1393,7 +1393,7 @@ cudaError_t launch_anneal(const AnnealArgs &a, int cluster_size, cudaStream_t st
     if (a.proposal == 0) {
         // CLV_ANNEAL_VARIANT=9: the phase-profiling build of the headline mode
         switch (env_int("CLV_ANNEAL_VARIANT", 0)) {
-            case 9: return launch_mode<MODE_BEST_ALL, 3, 2, true>(a, cluster_size, st);
+            case 9: return launch_mode<MODE_BEST_ALL, 2, 2, true>(a, cluster_size, st);
             default: return launch_mode<MODE_BEST_ALL, 2, 2>(a, cluster_size, st);
         }
     }
