@@ -1397,8 +1397,8 @@ cudaError_t launch_anneal(const AnnealArgs &a, int cluster_size, cudaStream_t st
             default: return launch_mode<MODE_BEST_ALL, 2, 2>(a, cluster_size, st);
         }
     }
-    if (a.evaluate == 0) return launch_mode<MODE_UNIFORM_ALL, 3, 1>(a, cluster_size, st);
-    return launch_mode<MODE_UNIFORM_PROPOSAL, 3, 1>(a, cluster_size, st);
+    if (a.evaluate == 0) return launch_mode<MODE_UNIFORM_ALL, 2, 1>(a, cluster_size, st);
+    return launch_mode<MODE_UNIFORM_PROPOSAL, 2, 1>(a, cluster_size, st);
 }
 
 }  // namespace clv
