@@ -29,7 +29,7 @@ st = bench.make_starts(prof, bench.SEED, 0, 128, 0.75)
 ap = bench.anneal_params(256)
 lib = N.load()
 lib.clv_debug_anneal_profile.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-cl = int(os.environ.get("CLV_PROFILE_CLUSTER", "3"))
+cl = int(os.environ.get("CLV_PROFILE_CLUSTER", "2"))   # the auto size at 128 chains
 b = eng.anneal(st, prof, sc, ap, 1, cluster=cl)
 torch.cuda.synchronize()
 steps = b.host()["results"]["steps"].astype(np.float64)
