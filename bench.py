@@ -732,7 +732,7 @@ def run_other(args, rank, world, local):
         eng.build_feasibility(N_FLEET)
         rate = S.calibrate_arrival_rate(base_config(N_FLEET, prof), prof, 0.7)
         w = S.Workload(rate, 600.0, SEED)
-        C = args.chains * 8
+        C = args.chains * 32                    # 4096 fleets: 512 CTAs of 8 warps (1024 fleets left the GPU 0.3 waves)
         fleets = [f for f in __import__("paper_2304_09781_b200.search", fromlist=["random_fleets"]).random_fleets(
             eng, prof, N_FLEET, SEED, C, rank * C)]
         edges = [S.fleet_instances(f, prof) for f in fleets]
