@@ -39,7 +39,7 @@ constexpr int MAXP = CLV_MAX_EDGES * (CLV_MAX_EDGES + 1) / 2;   // 820 removal p
 constexpr int MAXCL = 16;
 constexpr long long NOIDX = -1;
 constexpr int NO_TOP = CLV_MAX_EDGES;     // lat_by_rank[NO_TOP] == 0: nothing left present
-constexpr int SCREEN_UNR = 2;             // candidates per lane per screen iteration
+constexpr int SCREEN_UNR = 3;             // candidates per lane per screen iteration
 constexpr int QCAP = 32 * (SCREEN_UNR + 1);   // per-warp queue: < 32 left + one iteration's survivors
 
 enum { MODE_BEST_ALL = 0, MODE_UNIFORM_ALL = 1, MODE_UNIFORM_PROPOSAL = 2 };
