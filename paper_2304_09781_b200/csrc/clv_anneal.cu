@@ -119,6 +119,7 @@ struct __align__(16) AnnealSmem {
     unsigned char sl[CLV_MAX_EDGES];       // slice kind of the edge
     unsigned short pair_tab[MAXP];         // P -> (x | y << 8)
     unsigned char pair_len[MAXP];          // static move-list lengths (staged from FamilyTables)
+    int pair_off[MAXP];                    // static move-list offsets (staged: off prepare's global loads)
     double ub[CLV_MAX_EDGES];              // per latency rank: c20 / (svc + W0_bound(m)) (pessimistic walk)
     double Cd[CLV_MAX_EDGES];              // centre's pessimistic tail at its i-th highest present rank
     unsigned char dr[CLV_MAX_EDGES];       // centre's present ranks, descending
@@ -591,7 +592,7 @@ __device__ __forceinline__ void prepare_step(AnnealSmem &s, RemEnt *rp, int E, i
         r.k1 = s.rk[x]; r.k2 = s.rk[y];
         r.ibase = E * E + p * NP;
         r.pre = lpos;
-        r.offm = __ldg(T.pair_off + p) - lpos;
+        r.offm = s.pair_off[p] - lpos;
         lpos += s.pair_len[p];
         r.end = lpos;
         pess_bounds(s, r.k1, r.k2, slo, r.penU, r.penL);
@@ -957,7 +958,7 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         s.er[e] = T.edge_by_rank[e];
         s.sl[e] = (unsigned char)(e % 5);
     }
-    for (int p = tid; p < E * (E + 1) / 2; p += ANT) s.pair_len[p] = T.pair_len[p];
+    for (int p = tid; p < E * (E + 1) / 2; p += ANT) { s.pair_len[p] = T.pair_len[p]; s.pair_off[p] = T.pair_off[p]; }
     for (int x = tid; x < E; x += ANT)
         for (int y = x; y < E; ++y) s.pair_tab[x * E - (x * (x - 1)) / 2 + (y - x)] = (unsigned short)(x | (y << 8));
     if (tid == 0) {
