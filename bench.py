@@ -36,7 +36,8 @@ sys.path.insert(0, ROOT)
 METRIC = "candidate configs scored/sec (objective+SLA) at 1/2/4/8 B200; re-plan time-to-solution"
 UNIT = "candidates/s"
 N_FLEET = 64
-CHAINS_PER_GPU = 128
+CHAINS_PER_GPU = 128          # c3 / des: chains (fleets) per GPU
+C2_CHAINS = 1024              # c2: the whole job's annealing chains (BASELINE configs[2]), split over the GPUs
 FAMILY = "efficientnet"
 LAMBDA = 0.5
 CI = 350.0
@@ -50,7 +51,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="clover", choices=["clover", "reference"])
-    ap.add_argument("--chains", type=int, default=CHAINS_PER_GPU)
+    ap.add_argument("--chains", type=int, default=CHAINS_PER_GPU, help="c3 / des: chains per GPU")
+    ap.add_argument("--c2-chains", type=int, default=C2_CHAINS,
+                    help="c2: annealing chains of the whole re-plan, sharded over the GPUs (strong scaling)")
+    ap.add_argument("--cpu-replan-chains", type=int, default=128,
+                    help="c2: chains of the timed re-plan that the all-core CPU leg re-runs (parity + CPU TTS)")
     ap.add_argument("--cluster", type=int, default=0, help="CTAs per chain (0 = auto: one wave)")
     ap.add_argument("--max-steps", type=int, default=256)
     ap.add_argument("--keep", type=float, default=0.75, help="c2 starts: P(GPU keeps the incumbent partition)")
@@ -312,7 +317,7 @@ def run_reference(args, rank, world):
     value = total_evals / total_time
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * total_time / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": _config(args, world, cores_chains=cores),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                              "sample": "%d chains per step (one per core), n=%d, V=7, oracle/anneal.py" % (cores, N_FLEET)},
@@ -321,14 +326,16 @@ def run_reference(args, rank, world):
 
 
 def _config(args, world, cores_chains=None):
+    per = (args.c2_chains // world) if cores_chains is None else cores_chains
     return {"workload": "c2: n=%d-GPU fleet, %s B1-B7 (V=7), lambda=%.1f, ci=%.0f gCO2/kWh, %d annealing chains "
-                        "per %s from perturbations of the incumbent (BASE) deployment (keep %.2f), full GED<=4 "
+                        "(%s) from perturbations of the incumbent (BASE) deployment (keep %.2f), full GED<=4 "
                         "neighbourhood scored per step, run to termination (stall 5, <=%d steps); one step = one "
                         "re-plan of all chains"
-                        % (N_FLEET, FAMILY, LAMBDA, CI, args.chains if cores_chains is None else cores_chains,
-                           "B200" if cores_chains is None else "CPU step", args.keep, args.max_steps),
-            "fleet_gpus": N_FLEET, "variants": 7, "chains_per_gpu": args.chains if cores_chains is None else cores_chains,
-            "chains_total": (args.chains * world) if cores_chains is None else cores_chains,
+                        % (N_FLEET, FAMILY, LAMBDA, CI, args.c2_chains if cores_chains is None else cores_chains,
+                           ("the whole re-plan, %d per GPU" % per) if cores_chains is None else "per CPU step",
+                           args.keep, args.max_steps),
+            "fleet_gpus": N_FLEET, "variants": 7, "chains_per_gpu": per,
+            "chains_total": args.c2_chains if cores_chains is None else cores_chains,
             "proposal": "best-h neighbour", "parallelism": "chains sharded across %d GPU(s), dp%d" % (world, world),
             "l2": "flushed between steps (256 MiB write outside the timed events)"}
 
@@ -363,7 +370,9 @@ def main():
     eng = CloverEngine(device=local, n_max=N_FLEET)
     sc = eng.calibrate(prof, N_FLEET, CI, LAMBDA)
     ap = anneal_params(args.max_steps)
-    C = args.chains
+    if args.c2_chains % world:
+        raise SystemExit("--c2-chains must be a multiple of the GPU count")
+    C = args.c2_chains // world                  # this rank's shard of the re-plan's chains
     total_steps = args.warmup + args.steps
     base = rank * C
     # chains of step s, rank r are candidates [s*C*world + r*C, ...) of the counter-RNG stream
@@ -480,7 +489,9 @@ def main():
         except Exception as exc:  # pragma: no cover
             k_src = "walk sample failed: %s" % exc
         if not args.no_cpu_replan:
-            cpu_tts, outs = cpu_replan(starts[args.warmup], SEED + args.warmup, args.max_steps)
+            kc = min(C, args.cpu_replan_chains)
+            cpu_tts, outs = cpu_replan(starts[args.warmup][:kc], SEED + args.warmup, args.max_steps)
+            cpu_tts["sample"] = "the first %d of the timed re-plan's %d chains on all host cores" % (kc, C)
             parity = chain_parity(outs, batches[args.warmup])
     e_nz = edge_evals / max(evals, 1)
     fl = flops_per_candidate(e_nz, k_walk)
@@ -515,7 +526,7 @@ def main():
     launches_per_step = 2 + (1 if world > 1 else 0)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * dev_time / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(args, world), "clocks": clk,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": ("search.anneal_chains -> clv_replan (one C-ABI call: pinned host starts H2D, anneal, "

@@ -1,9 +1,10 @@
 """Parity at the exact shapes the benchmark times (BASELINE.json configs[2..4]).
 
-* c2: the headline launch -- 128 chains of the n = 64 EfficientNet fleet from the bench's
-  incumbent perturbations, auto cluster size, max_steps 256 (chains run to the stall rule),
-  the single-scenario branch-free-division instantiation -- every chain bit for bit against
-  oracle/anneal.py.
+* c2: the per-GPU shard of the 8-GPU run -- 128 chains of the n = 64 EfficientNet fleet from the
+  bench's incumbent perturbations, auto cluster size, max_steps 256 (chains run to the stall
+  rule), the single-scenario branch-free-division instantiation -- every chain bit for bit
+  against oracle/anneal.py; and the default bench launch, the whole 1024-chain
+  re-plan on one GPU, its first and last 64 chains.
 * c3: the trace controller at n = 64 with 128 chains per re-plan over 6 h of the synthetic
   trace (72 ticks), against oracle/controller.py.
 * c4: 10^4 contiguous indices of the two-pod (ResNet / BERT) sweep at 128 GPUs per pod
@@ -46,6 +47,38 @@ def test_c2_headline_launch_all_chains(engine):
     res = batch.host()["results"]
     assert (res["status"] == 1).all()                 # every chain converged (stall rule)
     assert res["sla_met"].mean() > 0.5
+
+
+def test_c2_whole_replan_1024_chains(engine, feas64):
+    """The default bench launch: all 1024 chains of c2 on one B200 (cluster size 1, several
+    waves).  Chains from the first and the last waves (ids 0-63 and 960-1023) bit for bit
+    against oracle/anneal.py."""
+    import bench
+    from oracle.tables import OracleTables
+    from paper_2304_09781_b200.profiles import synthetic_profile
+    prof = synthetic_profile(bench.FAMILY)
+    T = OracleTables.from_profile(prof)
+    sc = engine.calibrate(prof, bench.N_FLEET, bench.CI, bench.LAMBDA)
+    from oracle.evaluator import calibrate
+    osc = calibrate(prof, T, bench.N_FLEET, bench.CI, bench.LAMBDA)
+    ap = bench.anneal_params(256)
+    C = bench.C2_CHAINS
+    starts = bench.make_starts(prof, bench.SEED, 3 * C, C, 0.75)          # the bench's first timed step
+    seed = bench.SEED + 3
+    h = engine.anneal(starts, prof, sc, ap, seed, chain_base=0, cluster=0).host()
+    ids = list(range(64)) + list(range(C - 64, C))
+    _G["feas"] = feas64
+    with _pool() as pool:
+        outs = pool.map(_chain_job, [(starts[c].astype(np.int64), bench.N_FLEET, T, osc, ap, seed, c) for c in ids],
+                        chunksize=1)
+    u64 = lambda x: np.float64(x).view(np.uint64)
+    for c, o in zip(ids, outs):
+        r = h["results"][c]
+        assert (int(r["status"]), int(r["steps"]), int(r["evals"]), int(r["best_index"])) == \
+            (o.status, o.steps, o.evals, o.best_idx), c
+        assert np.array_equal(h["best_w"][c].astype(np.int64), o.best_w), c
+        assert np.array_equal(h["final_w"][c].astype(np.int64), o.final_w), c
+        assert u64(r["h"]) == u64(o.best["h"]) and u64(r["p95_ms"]) == u64(o.best["L"]), c
 
 
 def test_c3_trace_n64_128_chains_6h(engine, feas64):
