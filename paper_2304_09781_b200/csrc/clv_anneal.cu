@@ -154,6 +154,7 @@ struct __align__(16) AnnealSmem {
     KRec slS[2][MAXCL], slV[2][MAXCL], slP[2][MAXCL];   // [step parity][cluster rank]
     unsigned long long slc[2][MAXCL];
     int dec_done;
+    int next_chain;                        // persistent launches: the chain this CTA works on
     unsigned long long prof_surv;          // debug profile: candidates scored in full
     unsigned long long prof_surv1;         // debug profile: of which singles and unit moves
     int bw[CLV_MAX_EDGES];                 // best graph (rank 0)
@@ -935,8 +936,21 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = (int)cluster.num_blocks();
     const int crank = (int)cluster.block_rank();
-    const int chain = blockIdx.x / CL;
-    if (chain >= args.n_chains) return;      // whole cluster exits together
+    // One chain per cluster; with single-CTA clusters and more chains than resident CTAs the
+    // launch is persistent: each CTA takes chains from a global counter until none are left
+    // (no wave quantisation; chains of different lengths balance).
+    const bool persistent = CL == 1 && args.chain_counter != nullptr;
+    int chain = persistent ? -1 : (int)(blockIdx.x / CL);
+    for (;;) {
+    if (persistent) {
+        __syncthreads();                     // the previous chain's shared state is no longer read
+        if (threadIdx.x == 0) s.next_chain = atomicAdd(args.chain_counter, 1);
+        __syncthreads();
+        chain = s.next_chain;
+    } else if (chain < 0) {
+        break;                               // the cluster's one chain is done
+    }
+    if (chain >= args.n_chains) break;       // whole cluster exits together
     const uint64_t gchain = (uint64_t)(args.chain_base + chain);
     const FamilyTables &T = *args.fam;
     const int E = T.E;
@@ -1306,6 +1320,8 @@ __global__ void __launch_bounds__(ANT, MINB) anneal_kernel(const __grid_constant
         r.best_index = best_idx; r.evals = evals; r.edge_evals = edge_evals;
         args.res[chain] = r;
     }
+    if (!persistent) chain = -1;
+    }   // chains of this CTA
 }
 
 template <int MODE, int MINB, int UNR, bool PROF = false>
@@ -1382,7 +1398,23 @@ static cudaError_t launch_mode(const AnnealArgs &a, int cluster_size, cudaStream
     }
     cfg.gridDim = dim3((unsigned)(a.n_chains * cluster_size), 1, 1);
     attr[0].val.clusterDim.x = (unsigned)cluster_size;
-    return cudaLaunchKernelEx(&cfg, kern, a);
+    AnnealArgs b = a;
+    b.chain_counter = nullptr;
+    if (cluster_size == 1 && a.chain_counter) {
+        // more chains than resident CTAs: a persistent grid of resident CTAs taking chains from
+        // a counter (no wave tail); otherwise one CTA per chain
+        int sms = 148, occ = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ANT, smem) == cudaSuccess && occ > 0 &&
+            a.n_chains > occ * sms) {
+            cfg.gridDim = dim3((unsigned)(occ * sms), 1, 1);
+            cudaError_t e = cudaMemsetAsync(a.chain_counter, 0, sizeof(int), st);
+            if (e != cudaSuccess) return e;
+            b.chain_counter = a.chain_counter;
+        }
+        cudaGetLastError();
+    }
+    return cudaLaunchKernelEx(&cfg, kern, b);
 }
 
 static int env_int(const char *name, int dflt) {

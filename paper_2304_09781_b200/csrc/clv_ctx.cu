@@ -180,7 +180,7 @@ void clv_destroy(clv_ctx *ctx) {
     cudaFree(ctx->ec_dev); cudaFree(ctx->small_dev);
     for (int f = 0; f < CLV_MAX_FAMILIES; ++f) cudaFree(ctx->pair_list_dev[f]);
     clv::sim_destroy(ctx->sim);
-    cudaFree(ctx->mvlog); cudaFree(ctx->replan_buf);
+    cudaFree(ctx->mvlog); cudaFree(ctx->replan_buf); cudaFree(ctx->chain_counter);
     delete ctx;
 }
 
@@ -609,6 +609,8 @@ int clv_anneal(clv_ctx *ctx, int family, int n, int n_chains, int64_t chain_base
             ctx->mvlog_cap = need;
         }
         a.mvlog = ctx->mvlog;
+        if (!ctx->chain_counter) CLV_CUDA(cudaMalloc(&ctx->chain_counter, sizeof(int)), "alloc chain counter");
+        a.chain_counter = ctx->chain_counter;    // used (and zeroed) only by persistent launches
     }
     {
         // debug phase profile buffer (CLV_ANNEAL_VARIANT=9 only)

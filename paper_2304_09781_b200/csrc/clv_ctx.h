@@ -46,6 +46,7 @@ struct clv_ctx {
     int32_t *small_dev = nullptr;             // realize scratch
     clv::SimState *sim = nullptr;             // serving simulator (clv_sim.cu)
     int *mvlog = nullptr;                     // chain move logs (best-graph reconstruction)
+    int *chain_counter = nullptr;             // persistent chain launches: next chain (one int)
     size_t mvlog_cap = 0;
     unsigned char *replan_buf = nullptr;      // clv_replan device staging: starts | results | best | final | record
     size_t replan_cap = 0;

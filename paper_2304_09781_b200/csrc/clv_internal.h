@@ -145,6 +145,7 @@ struct AnnealArgs {
     uint16_t *final_w;
     clv_log_row *log;
     int *mvlog;                     // [n_chains][max_steps] accepted move per step (-1 = none)
+    int *chain_counter;             // persistent launches: next chain to take (zeroed per launch); else null
     long long *prof;                // optional phase profile (debug variant only)
 };
 
