@@ -7,9 +7,9 @@ from paper_2304_09781_b200.engine import CloverEngine
 from paper_2304_09781_b200.profiles import synthetic_profile
 from paper_2304_09781_b200.search import anneal_chains
 eng = CloverEngine(n_max=64); prof = synthetic_profile("efficientnet")
-sc = eng.calibrate(prof, 64, 350.0, 0.5)
+sc = eng.calibrate(prof, bench.N_FLEET, bench.CI, bench.LAMBDA)
 ap = bench.anneal_params(64)
-st = [bench.make_starts(eng, prof, bench.SEED, i * 128, 128) for i in range(12)]
+st = [bench.make_starts(prof, bench.SEED, i * 128, 128, 0.75) for i in range(12)]
 for i in range(3): anneal_chains(eng, st[i], prof, sc, ap, i)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
