@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(SNT) score_graphs_kernel(const __grid_constant
 // slice counts and the latency-rank presence mask; the idle row is per slice,
 // so S_idle = sum_s count_s * idle_s after the loop.  The p95 walk reads the
 // candidate's weights back from the staged tile.
-constexpr int GS = 3;                       // pipeline stages
+constexpr int GS = 2;                       // pipeline stages (2 x 35 KB: 3 CTAs per SM)
 constexpr int CPT = 2;                      // candidates per thread
 constexpr int GT = SNT * CPT;               // candidates per tile
 
@@ -193,7 +193,7 @@ struct GraphRows {
 };
 
 template <int V, bool FAST>
-__global__ void __launch_bounds__(SNT) score_graphs_tma_kernel(const __grid_constant__ ScoreArgs a,
+__global__ void __launch_bounds__(SNT, 3) score_graphs_tma_kernel(const __grid_constant__ ScoreArgs a,
                                                                const __grid_constant__ GraphRows R) {
     constexpr int E = V * CLV_K;
     extern __shared__ __align__(128) unsigned char gsm[];
